@@ -1,0 +1,305 @@
+"""Benchmark: CG GDOF/s (N=7, FP64) and time per CG iteration.
+
+Workload (BASELINE.json configs[2]/[3]): Poisson PCG
+(h1=1, h2=0, Jacobi on the assembled diagonal, multiplicity-weighted dots) on
+the 64^3-element deformed unit box (a = 0.05), N = 7 -- 262,144 elements,
+134,217,728 local nodes -- solved from a zero initial guess.  One "step" is
+one PCG solve run for a fixed ITERS iterations (tolerance 0, so every step
+does identical work).  GDOF/s counts local nodes, E*(N+1)^3 * iterations /
+seconds (proj/src/bench.cpp:168).  Multi-GPU: the same mesh partitioned by
+RCB across the ranks (strong scaling).
+
+Arms:
+  default            our CUDA path (libsbx.so).  `value`: device-resident
+                     b/x, CUDA-event timed; `e2e`: the C-ABI call with pinned
+                     HOST b/x (H2D of b and x0, D2H of x inside the timing).
+  --impl reference   the reference's own CPU pcg (oracle/_ref, compiled from
+                     /root/reference, all host threads) on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "CG GDOF/s (N=7, FP64, Poisson PCG+Jacobi, deformed box)"
+UNIT = "GDOF/s"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                      f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--elements", type=int, nargs=3, default=[64, 64, 64])
+    ap.add_argument("--degree", type=int, default=7)
+    ap.add_argument("--iters", type=int, default=100, help="CG iterations per step")
+    ap.add_argument("--deform", type=float, default=0.05)
+    ap.add_argument("--cpu-sample", type=int, nargs=3, default=[32, 32, 32],
+                    help="mesh of the bounded CPU-baseline sample")
+    ap.add_argument("--cpu-iters", type=int, default=30)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# --------------------------------------------------------------- CPU arm --
+def cpu_reference_run(ex, ey, ez, N, deform, iters, steps, warmup):
+    """The reference's pcg (oracle/_ref: sembox compiled unmodified) on all host
+    threads.  Returns per-step seconds and metadata."""
+    from oracle import oracle as O
+
+    O.build(ref=True) if not O.ref_available() and os.path.isdir("/root/reference") else None
+    backend = "ref" if O.ref_available() else "port"
+    cores = os.cpu_count() or 1
+    if backend == "ref":
+        O._ref().ref_set_workers(cores)
+    cr = O.box_corners(ex, ey, ez, deform=deform)
+    P = O.Problem(ex, ey, ez, N, corners=cr, backend=backend)
+    b = P.rhs_random_continuous(77)
+    times = []
+    for s in range(warmup + steps):
+        t0 = time.perf_counter()
+        r = P.pcg(b, 1.0, 0.0, "jacobi", 0.0, iters)
+        dt = time.perf_counter() - t0
+        if s >= warmup:
+            times.append(dt)
+        assert r.iterations == iters, (r.iterations, iters)
+    return times, backend, (cores if backend == "ref" else 1), P.nodes_count
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    ex, ey, ez = args.cpu_sample
+    N = args.degree
+    iters = args.cpu_iters
+    times, backend, cores, nodes = cpu_reference_run(ex, ey, ez, N, args.deform, iters,
+                                                     max(args.steps, 1), 1)
+    t = statistics.median(times)
+    val = nodes * iters / t / 1e9
+    sample = (f"{ex}x{ey}x{ez} deformed box N={N}, {iters} PCG iterations per step "
+              f"(bounded sample of the {args.elements[0]}x{args.elements[1]}x{args.elements[2]} "
+              f"workload; GDOF/s is per local node and iteration)")
+    line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": len(times), "warmup": 1, "ms_per_step": t * 1e3,
+            "ms_per_iteration": t * 1e3 / iters, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": "Poisson PCG, Jacobi, deformed box (a=0.05)",
+                       "elements": [ex, ey, ez], "degree": N, "iterations_per_step": iters},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores,
+                             "kind": "reference" if backend == "ref" else "port",
+                             "sample": sample},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------- GPU arm --
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import paper_2109_03592_b200 as sb
+
+    rank, world, local = dist_env()
+    if world > 1:
+        from paper_2109_03592_b200 import dist
+
+        return dist.bench_main(args)
+    torch.cuda.set_device(local)
+    ex, ey, ez = args.elements
+    N = args.degree
+    iters = args.iters
+    t_setup = time.perf_counter()
+    ctx = sb.Context.box(ex, ey, ez, N, deform=args.deform, device=local)
+    t_setup = time.perf_counter() - t_setup
+    nodes = ctx.nodes
+    op = sb.HelmholtzOperator(ctx, sb.HelmholtzCoeffs(1.0, 0.0))
+    # continuous masked RHS (test_schwarz.cpp:30-38 recipe with a device RNG):
+    # random field -> gs_sum -> * inv_mult * mask
+    g = torch.Generator(device=f"cuda:{local}").manual_seed(77)
+    b = torch.rand(nodes, dtype=torch.float64, device=f"cuda:{local}", generator=g) * 2 - 1
+    sb.gs_sum_inplace(ctx, b)
+    inv = torch.from_numpy(ctx.array(1)).cuda(local)
+    mask = torch.from_numpy(ctx.array(0)).cuda(local)
+    b.mul_(inv * mask)
+    del inv, mask
+    x = torch.zeros_like(b)
+    cfg = sb.KrylovConfig(tolerance=0.0, max_iterations=iters)
+
+    def step_dev():
+        x.zero_()
+        return sb.pcg(op, b, x, cfg, history=False)
+
+    for _ in range(args.warmup):
+        r = step_dev()
+    assert r.iterations == iters
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record()
+        for _ in range(args.steps):
+            step_dev()
+        ev1.record()
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    value = nodes * iters / (ms * 1e-3) / 1e9
+
+    # e2e: pinned host b/x through the C ABI, copies inside the timed region
+    hb = torch.empty(nodes, dtype=torch.float64, pin_memory=True)
+    hb.copy_(b)
+    hx = torch.zeros(nodes, dtype=torch.float64, pin_memory=True)
+
+    def step_host():
+        hx.zero_()
+        return sb.pcg(op, hb, hx, cfg, history=False)
+
+    step_host()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step_host()
+    torch.cuda.synchronize()
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    e2e_val = nodes * iters / (e2e_ms * 1e-3) / 1e9
+
+    # per-kernel device time (timing mode: same kernels, host-launched, events
+    # on the launching stream) -> roofline of the dominant kernel
+    ctx.enable_timing(True)
+    x.zero_()
+    sb.pcg(op, b, x, cfg, history=False)
+    ctx.enable_timing(False)
+    ax_ms, ax_n = ctx.kernel_time("ax")
+    up_ms, up_n = ctx.kernel_time("update")
+    peak, peak_kind = load_peaks()
+    n = N + 1
+    k1_bytes = 13 * 8 * nodes  # K1 reads r, dinv, p, x, g1..g6; writes p, x, w
+    k1_s = ax_ms / max(ax_n, 1) * 1e-3
+    achieved = k1_bytes / k1_s / 1e9
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    if os.path.exists(tfile):
+        try:
+            traffic = json.load(open(tfile)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "ms_per_iteration": ms / iters,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": "Poisson PCG, Jacobi, deformed box (a=0.05), zero guess",
+                       "elements": [ex, ey, ez], "degree": N, "local_nodes": nodes,
+                       "iterations_per_step": iters, "parallelism": "rcb1",
+                       "l2": "inputs larger than L2 (per-iteration working set "
+                             f"{nodes * 152 / 1e9:.1f} GB >> 126 MB)",
+                       "setup_s": round(t_setup, 2)},
+            "e2e": {"value": e2e_val, "unit": UNIT, "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": 2 * 8 * nodes, "d2h_bytes_per_step": 8 * nodes},
+            "gpu_launches": args.steps * (2 * iters + 6),
+            "roofline": {"bound": "hbm", "kernel": "cg_ax_kernel (K1: p-update + axhelm + p'Ap)",
+                         "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "algorithmic_bytes_per_node": 104, "k1_ms": k1_s * 1e3,
+                         "k2_ms": up_ms / max(up_n, 1),
+                         "k1_share": ax_ms / max(ax_ms + up_ms, 1e-12)},
+            "clocks": clk.summary()}
+    if not args.no_cpu_baseline:
+        cex, cey, cez = args.cpu_sample
+        times, backend, cores, cnodes = cpu_reference_run(cex, cey, cez, N, args.deform,
+                                                          args.cpu_iters, 1, 0)
+        t = statistics.median(times)
+        line["cpu_baseline"] = {
+            "value": cnodes * args.cpu_iters / t / 1e9, "unit": UNIT, "cores": cores,
+            "kind": "reference" if backend == "ref" else "port",
+            "sample": f"{cex}x{cey}x{cez} deformed box N={N}, {args.cpu_iters} PCG iterations "
+                      f"(reference sembox pcg, {cores} threads)",
+            "ms_per_iteration": t * 1e3 / args.cpu_iters}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

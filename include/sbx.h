@@ -1,0 +1,233 @@
+/*
+ * sbx.h -- C ABI of the B200-native spectral-element PCG hot path.
+ *
+ * Drop-in boundary for the reference's ("sembox", /root/reference/proj)
+ * operator API on the preconditioned-CG path.
+ * Plain pointers and sizes only: no C++ or torch types cross this boundary.
+ * Each entry point names the reference interface it replaces (file:line under
+ * /root/reference/proj).
+ *
+ * Data layout (identical to the reference, so host<->device copies are flat):
+ *   field  : E * n^3 doubles, index ((e*n + k)*n + j)*n + i, x fastest,
+ *            elements outermost                     (include/sembox/field.hpp:15-36)
+ *   deriv  : n*n row-major, D[i*n+j] = l_j'(x_i)     (include/sembox/basis.hpp:15)
+ *   g1..g6, bm : E*n^3 each (GeometricFactors SoA)   (include/sembox/operators.hpp:18-26)
+ *   gather-scatter map: group_offsets[G+1], group_nodes[E*n^3] (int64), groups
+ *            ascending by gid, copies ascending by local index (include/sembox/gather.hpp:14-29)
+ *
+ * Vector arguments of the operator/solver calls may be DEVICE pointers (the
+ * fast path) or HOST pointers (pageable or pinned; staged through the
+ * context's buffers) -- detected per call with cudaPointerGetAttributes.
+ *
+ * Errors: every call returns an sbx_status; sbx_last_error() gives the
+ * message (thread-local).  The codes map one-to-one onto the reference's
+ * exception taxonomy (include/sembox/errors.hpp:10-41).
+ *
+ * Threading: calls on one context are synchronous (stream-ordered inside,
+ * synchronised at return).  Distinct contexts may be used from distinct
+ * threads.  Results are deterministic for a fixed device count.
+ */
+#ifndef SBX_H
+#define SBX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SBX_OK = 0,
+  SBX_E_INVALID = 1,   /* null pointer / bad flag / bad handle                     */
+  SBX_E_CONFIG = 2,    /* sembox::ConfigError  (bad degree, bad rank count, ...)   */
+  SBX_E_SHAPE = 3,     /* sembox::ContractViolation (grid/shape/map mismatch)      */
+  SBX_E_MESH = 4,      /* sembox::MeshError (nonpositive Jacobian)                 */
+  SBX_E_BREAKDOWN = 5, /* sembox::SolverError: p'Ap <= 0 or non-finite (krylov.cpp:61-64) */
+  SBX_E_NAN = 6,       /* sembox::SolverError: residual NaN/Inf (krylov.cpp:72-75)  */
+  SBX_E_CUDA = 7,      /* CUDA runtime failure                                      */
+  SBX_E_COMM = 8,      /* NCCL / communicator failure                               */
+  SBX_E_NOMEM = 9      /* device allocation failed                                  */
+} sbx_status;
+
+/* operator flags */
+#define SBX_FLAG_EXACT 0x1u  /* reference evaluation order, no FMA: bitwise equal to sembox */
+#define SBX_FLAG_FLIP_T 0x2u /* debug::axhelm_sign_flip (operators.hpp:114-118, operators.cpp:221) */
+#define SBX_FLAG_NO_MASK 0x4u /* HelmholtzOperator with mask == nullptr (operators.hpp:107) */
+
+const char* sbx_last_error(void);
+const char* sbx_version(void);
+
+/* ------------------------------------------------------------ host setup --
+ * Host-side builders of the operator inputs.  The product's own C++ (not the
+ * reference); bitwise equal to the reference builders (tests/test_setup.py). */
+
+/* build_gll_basis (basis.cpp:60-112): nodes[n], weights[n], deriv[n*n]. */
+sbx_status sbx_gll_basis(int degree, double* nodes, double* weights, double* deriv);
+
+/* build_box_mesh corners (mesh.cpp:21-52): corners[E][8][3]. */
+sbx_status sbx_box_corners(int ex, int ey, int ez, const double origin[3],
+                           const double lengths[3], double* corners);
+
+/* conforming sin-bump deformation of the benchmark meshes. */
+sbx_status sbx_deform_corners(int64_t elem_count, double amplitude, double* corners);
+
+/* build_geometric_factors (operators.cpp:123-178).  Any of the outputs may be
+ * NULL.  *bad_elem = -1, or the first element with detJ <= 0 (SBX_E_MESH). */
+sbx_status sbx_geometric_factors(int64_t elem_count, int degree, const double* corners,
+                                 double* g1, double* g2, double* g3, double* g4,
+                                 double* g5, double* g6, double* bm, double* jac,
+                                 int64_t* bad_elem);
+
+/* build_gather_scatter (gather.cpp:10-83) for a structured box.  gid, mult,
+ * inv_mult may be NULL; group_offsets needs room for nodes+1 entries.
+ * *global_count receives G. */
+sbx_status sbx_gather_scatter(int ex, int ey, int ez, const int periodic[3], int degree,
+                              int64_t* gid, int64_t* group_offsets, int64_t* group_nodes,
+                              int32_t* mult, double* inv_mult, int64_t* global_count);
+
+/* build_dirichlet_mask (operators.cpp:433-455). */
+sbx_status sbx_dirichlet_mask(int ex, int ey, int ez, const int periodic[3], int degree,
+                              double* mask);
+
+/* partition_rcb (mesh.cpp:168-226): rank_of[E]. */
+sbx_status sbx_partition_rcb(int64_t elem_count, const double* corners, int ranks,
+                             int32_t* rank_of);
+
+/* ------------------------------------------------------------ context ----- */
+typedef struct sbx_ctx sbx_ctx;
+
+/* Everything HelmholtzOperator holds (operators.hpp:103-108), as host arrays
+ * in the reference layout.  Uploaded and re-laid-out for the device once. */
+typedef struct {
+  int64_t elem_count;           /* E (this rank's elements)                       */
+  int32_t degree;               /* N (n = N+1 points per direction)               */
+  const double* deriv;          /* n*n                                            */
+  const double* g[6];           /* g1..g6                                         */
+  const double* bm;             /* may be NULL when only h2 == 0 is used          */
+  const double* mask;           /* may be NULL: no Dirichlet mask                 */
+  int64_t global_count;         /* G                                              */
+  const int64_t* group_offsets; /* G+1                                            */
+  const int64_t* group_nodes;   /* E*n^3                                          */
+} sbx_problem_desc;
+
+sbx_status sbx_ctx_create(const sbx_problem_desc* desc, int device, sbx_ctx** out);
+
+/* Product-native setup of a structured (optionally deformed) box: builds
+ * corners, G, gs map, mask with the builders above (multi-threaded host) and
+ * uploads them.  periodic[3]; amplitude 0 = undeformed. */
+typedef struct {
+  int ex, ey, ez;
+  int degree;
+  int periodic[3];
+  double origin[3];
+  double lengths[3];
+  double deform_amplitude;
+} sbx_box_desc;
+
+sbx_status sbx_ctx_create_box(const sbx_box_desc* desc, int device, sbx_ctx** out);
+
+void sbx_ctx_destroy(sbx_ctx* ctx);
+
+/* E, n, local nodes, G, device bytes */
+sbx_status sbx_ctx_info(const sbx_ctx* ctx, int64_t* elem_count, int32_t* n1d,
+                        int64_t* nodes, int64_t* global_count, int64_t* device_bytes);
+
+/* copy context-owned arrays (reference layout) to host or device memory:
+ * which = 0 mask, 1 inv_mult, 2 bm, 3..8 g1..g6, 9 deriv */
+sbx_status sbx_ctx_copy_array(const sbx_ctx* ctx, int which, double* out);
+
+/* Launch stream (cudaStream_t as void*); NULL = the context's own stream. */
+sbx_status sbx_ctx_set_stream(sbx_ctx* ctx, void* stream);
+
+/* ------------------------------------------------------------ operators --- */
+
+/* axhelm (operators.hpp:59-60, operators.cpp:215-263): w = D^T G D u h1 + h2 bm u */
+sbx_status sbx_axhelm(sbx_ctx* ctx, const double* u, double* w, double h1, double h2,
+                      uint32_t flags);
+
+/* axhelm_diagonal (operators.cpp:272-298); assembled != 0 adds gs_sum
+ * (HelmholtzOperator::assembled_diagonal, operators.cpp:536-540). */
+sbx_status sbx_axhelm_diagonal(sbx_ctx* ctx, double h1, double h2, int assembled,
+                               double* diag);
+
+/* gs_sum_inplace (gather.hpp:39, gather.cpp:85-98), bitwise equal. */
+sbx_status sbx_gs_sum(sbx_ctx* ctx, double* field);
+
+/* HelmholtzOperator::apply (operators.hpp:110, operators.cpp:530-534):
+ * q = mask * gs_sum(axhelm(x)). */
+sbx_status sbx_apply(sbx_ctx* ctx, const double* x, double* q, double h1, double h2,
+                     uint32_t flags);
+
+/* field_dot_weighted (field.hpp:60-62, field.cpp:69-81); weighted = 0 gives
+ * field_dot.  SBX_FLAG_EXACT reproduces the reference's summation order. */
+sbx_status sbx_dot(sbx_ctx* ctx, const double* a, const double* b, int weighted,
+                   uint32_t flags, double* result);
+
+/* --------------------------------------------------------------- solver --- */
+typedef enum { SBX_PRECOND_NONE = 0, SBX_PRECOND_JACOBI = 1 } sbx_precond;
+
+typedef enum {
+  SBX_MODE_EXACT = 0, /* reference operation order; bitwise equal residual history   */
+  SBX_MODE_FAST = 1   /* fused kernels, device-resident scalars, CUDA graph          */
+} sbx_mode;
+
+/* KrylovConfig (krylov.hpp:18-22) + the operator/preconditioner choice. */
+typedef struct {
+  double tolerance;       /* relative residual (default 1e-8)                      */
+  int32_t max_iterations; /* default 500                                           */
+  int32_t precond;        /* sbx_precond                                           */
+  int32_t mode;           /* sbx_mode                                              */
+  double h1, h2;          /* HelmholtzCoeffs (operators.hpp:39-44), scalars          */
+  double* history;        /* host, optional: relative residual per iteration         */
+  int64_t history_capacity;
+} sbx_pcg_config;
+
+/* PcgResult (krylov.hpp:24-30) + error iteration (SolverError::iteration). */
+typedef struct {
+  int32_t iterations;
+  int32_t converged;
+  double rel_residual;
+  double rel_residual_precond;
+  int32_t error_iteration; /* -1 unless SBX_E_BREAKDOWN / SBX_E_NAN               */
+  int64_t history_length;  /* entries produced (may exceed capacity)              */
+} sbx_pcg_result;
+
+void sbx_pcg_config_default(sbx_pcg_config* cfg);
+
+/* pcg (krylov.hpp:38-40, krylov.cpp:7-91) on the assembled operator with the
+ * multiplicity-weighted dot and (optionally) Jacobi on assembled_diagonal().
+ * x carries the initial guess in and the solution out.  Reaching
+ * max_iterations is reported (converged = 0), not an error. */
+sbx_status sbx_pcg(sbx_ctx* ctx, const double* b, double* x, const sbx_pcg_config* cfg,
+                   sbx_pcg_result* result);
+
+/* -------------------------------------------------------- multi-GPU ------ */
+/* One process per GPU.  The application (or torch.distributed, see
+ * paper_2109_03592_b200/dist.py) distributes the 128-byte NCCL id from rank 0. */
+sbx_status sbx_comm_unique_id(uint8_t id[128]);
+
+/* Distributed context: this rank's elements of a structured box partitioned
+ * by partition_rcb (rank_of[E_global] as produced by sbx_partition_rcb).
+ * Builds the local map and the cross-rank gather-scatter exchange plan;
+ * requires an NCCL communicator (id from sbx_comm_unique_id on rank 0). */
+sbx_status sbx_ctx_create_box_dist(const sbx_box_desc* desc, const int32_t* rank_of,
+                                   int nranks, int rank, const uint8_t id[128], int device,
+                                   sbx_ctx** out);
+
+/* local element ids (global numbering, ascending) of a distributed context */
+sbx_status sbx_ctx_local_elements(const sbx_ctx* ctx, int64_t* global_ids);
+
+/* --------------------------------------------------------- instrumentation */
+/* Per-kernel device time of the last sbx_pcg call in FAST mode, measured with
+ * CUDA events on the launching stream when enabled (adds no sync inside the
+ * solve).  names: "ax", "gs", "update"; returns total ms and launch count. */
+sbx_status sbx_ctx_enable_timing(sbx_ctx* ctx, int enable);
+sbx_status sbx_ctx_kernel_time(const sbx_ctx* ctx, const char* name, double* total_ms,
+                               int64_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SBX_H */

@@ -1,0 +1,850 @@
+// C ABI (include/sbx.h): context lifetime, data upload/re-layout, operator
+// entry points and the two PCG drivers (EXACT: the reference's pcg loop with
+// device operators; FAST: fused kernels with device-resident scalars).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "cg.cuh"
+#include "kernels.cuh"
+#include "sbx_internal.h"
+
+namespace sbx {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+}  // namespace sbx
+
+using namespace sbx;
+
+#define SBX_CUDA(call)                                                              \
+  do {                                                                              \
+    cudaError_t _e = (call);                                                        \
+    if (_e != cudaSuccess) {                                                        \
+      set_error(std::string(#call) + ": " + cudaGetErrorString(_e));                \
+      return SBX_E_CUDA;                                                            \
+    }                                                                               \
+  } while (0)
+
+#define SBX_TRY(call)                     \
+  do {                                    \
+    sbx_status _s = (sbx_status)(call);   \
+    if (_s != SBX_OK) return _s;          \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+struct sbx_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;
+  OpDev op;
+  int64_t global_count = 0;
+  bool interior_clean = false;  // every element-interior node: unmasked singleton
+  bool has_mask = false;
+  std::vector<void*> allocs;
+  int64_t device_bytes = 0;
+  // host copies kept for re-layout queries
+  // scratch
+  double* work[6] = {};  // nodes-sized
+  double* partials = nullptr;
+  int64_t partials_len = 0;
+  double* dscal = nullptr;   // 16 device doubles
+  uint32_t* dcount = nullptr;
+  double* hscal = nullptr;   // pinned 16 doubles
+  // Jacobi diagonal cache
+  double* ddiag = nullptr;
+  double* ddinv = nullptr;
+  double diag_h1 = NAN, diag_h2 = NAN;
+  // fast CG
+  std::unique_ptr<CgEngine> cg;
+  // distributed (filled by sbx_ctx_create_box_dist)
+  std::vector<int64_t> local_elements;
+  // timing
+  bool timing = false;
+};
+
+namespace {
+
+sbx_status dalloc(sbx_ctx* c, void** p, size_t bytes) {
+  if (bytes == 0) bytes = 8;
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e != cudaSuccess) {
+    set_error(std::string("cudaMalloc(") + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? SBX_E_NOMEM : SBX_E_CUDA;
+  }
+  c->allocs.push_back(*p);
+  c->device_bytes += (int64_t)bytes;
+  return SBX_OK;
+}
+
+template <typename T>
+sbx_status dupload(sbx_ctx* c, T** out, const T* host, int64_t count) {
+  void* p = nullptr;
+  SBX_TRY(dalloc(c, &p, sizeof(T) * (size_t)count));
+  if (host && count > 0)
+    SBX_CUDA(cudaMemcpyAsync(p, host, sizeof(T) * (size_t)count, cudaMemcpyHostToDevice,
+                             c->stream));
+  *out = static_cast<T*>(p);
+  return SBX_OK;
+}
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+sbx_status work(sbx_ctx* c, int slot, double** out) {
+  if (!c->work[slot]) {
+    void* p = nullptr;
+    SBX_TRY(dalloc(c, &p, sizeof(double) * (size_t)c->op.nodes));
+    c->work[slot] = static_cast<double*>(p);
+  }
+  *out = c->work[slot];
+  return SBX_OK;
+}
+
+// Input/output staging: device pointers pass through, host pointers are copied
+// through a context work buffer.
+struct In {
+  const double* d = nullptr;
+};
+sbx_status stage_in(sbx_ctx* c, const double* p, int slot, const double** out) {
+  if (is_device_ptr(p)) {
+    *out = p;
+    return SBX_OK;
+  }
+  double* w = nullptr;
+  SBX_TRY(work(c, slot, &w));
+  SBX_CUDA(cudaMemcpyAsync(w, p, sizeof(double) * (size_t)c->op.nodes, cudaMemcpyHostToDevice,
+                           c->stream));
+  *out = w;
+  return SBX_OK;
+}
+
+sbx_status finish(sbx_ctx* c) {
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) {
+    set_error(std::string("kernel execution: ") + cudaGetErrorString(e));
+    return SBX_E_CUDA;
+  }
+  return SBX_OK;
+}
+
+// Boundary CSR: all groups except element-interior unmasked singletons.
+sbx_status build_boundary_csr(sbx_ctx* c, const int64_t* offsets, const int64_t* nodes,
+                              const double* mask) {
+  const int n = c->op.n;
+  const int64_t n3 = (int64_t)n * n * n, N = c->op.nodes, G = c->global_count;
+  if (offsets[0] != 0 || offsets[G] != N) {
+    set_error("gather-scatter map: group_offsets must start at 0 and end at E*n^3");
+    return SBX_E_SHAPE;
+  }
+  if (N >= (int64_t)INT32_MAX) {
+    set_error("gather-scatter map: more than 2^31-1 local nodes per device");
+    return SBX_E_SHAPE;
+  }
+  std::vector<uint8_t> seen(N, 0);
+  auto on_boundary = [&](int64_t a) {
+    const int64_t l = a % n3;
+    const int i = (int)(l % n), j = (int)((l / n) % n), k = (int)(l / ((int64_t)n * n));
+    return i == 0 || j == 0 || k == 0 || i == n - 1 || j == n - 1 || k == n - 1;
+  };
+  std::vector<int32_t> off;
+  std::vector<int32_t> idx;
+  off.reserve(G / 2 + 2);
+  idx.reserve(N * 6 / 10 + 16);
+  off.push_back(0);
+  bool clean = true;
+  std::vector<uint8_t> mult8(N, 0);
+  std::vector<double> inv_mult(N, 0.0);
+  for (int64_t g = 0; g < G; ++g) {
+    const int64_t lo = offsets[g], hi = offsets[g + 1];
+    if (hi <= lo || lo < 0 || hi > N) {
+      set_error("gather-scatter map: empty or out-of-range group " + std::to_string(g));
+      return SBX_E_SHAPE;
+    }
+    bool keep = hi - lo > 1;
+    for (int64_t q = lo; q < hi; ++q) {
+      const int64_t a = nodes[q];
+      if (a < 0 || a >= N || seen[a]) {
+        set_error("gather-scatter map: group_nodes is not a permutation of the local nodes");
+        return SBX_E_SHAPE;
+      }
+      seen[a] = 1;
+      const bool masked = mask && mask[a] == 0.0;
+      if (masked || on_boundary(a)) keep = true;
+      if (!on_boundary(a) && (masked || hi - lo > 1)) clean = false;
+      mult8[a] = (uint8_t)std::min<int64_t>(hi - lo, 255);
+      inv_mult[a] = 1.0 / (double)(int32_t)(hi - lo);
+    }
+    if (!keep) continue;
+    for (int64_t q = lo; q < hi; ++q) {
+      const int64_t a = nodes[q];
+      const bool masked = mask && mask[a] == 0.0;
+      idx.push_back(masked ? ~(int32_t)a : (int32_t)a);
+    }
+    off.push_back((int32_t)idx.size());
+  }
+  c->interior_clean = clean;
+  c->op.nB = (int64_t)off.size() - 1;
+  c->op.nBcopies = (int64_t)idx.size();
+  int32_t *doff = nullptr, *didx = nullptr;
+  SBX_TRY(dupload(c, &doff, off.data(), (int64_t)off.size()));
+  SBX_TRY(dupload(c, &didx, idx.data(), (int64_t)idx.size()));
+  c->op.b_off = doff;
+  c->op.b_idx = didx;
+  uint8_t* dm8 = nullptr;
+  double* dim = nullptr;
+  SBX_TRY(dupload(c, &dm8, mult8.data(), N));
+  SBX_TRY(dupload(c, &dim, inv_mult.data(), N));
+  c->op.mult8 = dm8;
+  c->op.inv_mult = dim;
+  SBX_CUDA(cudaStreamSynchronize(c->stream));  // host vectors die here
+  return SBX_OK;
+}
+
+sbx_status ctx_init_common(sbx_ctx* c, int device) {
+  c->device = device;
+  SBX_CUDA(cudaSetDevice(device));
+  SBX_CUDA(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+  c->stream = c->own_stream;
+  void* p = nullptr;
+  SBX_TRY(dalloc(c, &p, 64 * sizeof(double)));
+  c->dscal = static_cast<double*>(p);
+  SBX_TRY(dalloc(c, &p, 64 * sizeof(uint32_t)));
+  c->dcount = static_cast<uint32_t*>(p);
+  SBX_CUDA(cudaMemsetAsync(c->dcount, 0, 64 * sizeof(uint32_t), c->stream));
+  SBX_CUDA(cudaMallocHost(&c->hscal, 64 * sizeof(double)));
+  return SBX_OK;
+}
+
+sbx_status ensure_partials(sbx_ctx* c, int64_t count) {
+  if (c->partials_len >= count) return SBX_OK;
+  void* p = nullptr;
+  SBX_TRY(dalloc(c, &p, sizeof(double) * (size_t)count));
+  c->partials = static_cast<double*>(p);
+  c->partials_len = count;
+  return SBX_OK;
+}
+
+// Upload the problem (reference layout host arrays) and re-lay it out.
+sbx_status ctx_upload(sbx_ctx* c, const sbx_problem_desc* d) {
+  const int n = d->degree + 1;
+  c->op.E = d->elem_count;
+  c->op.n = n;
+  c->op.nodes = d->elem_count * (int64_t)n * n * n;
+  c->global_count = d->global_count;
+  for (int q = 0; q < n * n; ++q) c->op.Dh[q] = d->deriv[q];
+  double* dD = nullptr;
+  SBX_TRY(dupload(c, &dD, d->deriv, (int64_t)n * n));
+  c->op.Dd = dD;
+  const int64_t N = c->op.nodes;
+  // geometry: stage each SoA array once and pack to [E][6][n^3]
+  double* G = nullptr;
+  SBX_TRY(dupload<double>(c, &G, nullptr, 6 * N));
+  {
+    double* tmp[6] = {};
+    for (int q = 0; q < 6; ++q) {
+      SBX_CUDA(cudaMalloc(&tmp[q], sizeof(double) * (size_t)std::max<int64_t>(N, 1)));
+      SBX_CUDA(cudaMemcpyAsync(tmp[q], d->g[q], sizeof(double) * (size_t)N,
+                               cudaMemcpyHostToDevice, c->stream));
+    }
+    OpDev tmpop = c->op;
+    SBX_CUDA(launch_pack_geometry(tmpop, tmp, G, c->stream));
+    SBX_CUDA(cudaStreamSynchronize(c->stream));
+    for (int q = 0; q < 6; ++q) cudaFree(tmp[q]);
+  }
+  c->op.G = G;
+  if (d->bm) {
+    double* bm = nullptr;
+    SBX_TRY(dupload(c, &bm, d->bm, N));
+    c->op.bm = bm;
+  }
+  if (d->mask) {
+    double* m = nullptr;
+    SBX_TRY(dupload(c, &m, d->mask, N));
+    c->op.mask = m;
+    c->has_mask = true;
+  }
+  SBX_TRY(build_boundary_csr(c, d->group_offsets, d->group_nodes, d->mask));
+  SBX_TRY(ensure_partials(c, std::max<int64_t>(c->op.E, 4096)));
+  c->cg.reset(new CgEngine());
+  return SBX_OK;
+}
+
+sbx_status check_ctx(const sbx_ctx* c) {
+  if (!c) {
+    set_error("null context");
+    return SBX_E_INVALID;
+  }
+  return SBX_OK;
+}
+
+// ---- scalar helpers for the EXACT driver ---------------------------------
+sbx_status dot_exact(sbx_ctx* c, const double* a, const double* b, bool weighted, double* out) {
+  SBX_CUDA(launch_dot_exact(c->op, a, b, weighted ? c->op.inv_mult : nullptr, c->partials,
+                            c->dscal, c->stream));
+  SBX_CUDA(cudaMemcpyAsync(c->hscal, c->dscal, sizeof(double), cudaMemcpyDeviceToHost,
+                           c->stream));
+  SBX_TRY(finish(c));
+  *out = c->hscal[0];
+  return SBX_OK;
+}
+
+sbx_status apply_dev(sbx_ctx* c, const double* x, double* q, double h1, double h2,
+                     bool exact, bool flip, bool use_mask) {
+  SBX_CUDA(launch_axhelm(c->op, x, q, h1, h2, exact, flip, c->stream));
+  SBX_CUDA(launch_gs(c->op, q, use_mask && c->has_mask, c->stream));
+  return SBX_OK;
+}
+
+sbx_status ensure_diag(sbx_ctx* c, double h1, double h2) {
+  if (c->ddiag && c->diag_h1 == h1 && c->diag_h2 == h2) return SBX_OK;
+  if (!c->ddiag) {
+    void* p = nullptr;
+    SBX_TRY(dalloc(c, &p, sizeof(double) * (size_t)c->op.nodes));
+    c->ddiag = static_cast<double*>(p);
+    SBX_TRY(dalloc(c, &p, sizeof(double) * (size_t)c->op.nodes));
+    c->ddinv = static_cast<double*>(p);
+  }
+  SBX_CUDA(launch_axhelm_diag(c->op, h1, h2, c->ddiag, c->stream));
+  SBX_CUDA(launch_gs(c->op, c->ddiag, false, c->stream));
+  SBX_CUDA(launch_recip(c->op.nodes, c->ddiag, c->ddinv, c->stream));
+  c->diag_h1 = h1;
+  c->diag_h2 = h2;
+  return SBX_OK;
+}
+
+// ---- EXACT PCG: krylov.cpp:7-91 statement by statement ------------------
+sbx_status pcg_exact(sbx_ctx* c, const double* b, double* x, const sbx_pcg_config* cfg,
+                     sbx_pcg_result* res) {
+  const int64_t N = c->op.nodes;
+  cudaStream_t s = c->stream;
+  auto push = [&](double v) {
+    if (cfg->history && res->history_length < cfg->history_capacity)
+      cfg->history[res->history_length] = v;
+    ++res->history_length;
+  };
+  double bb;
+  SBX_TRY(dot_exact(c, b, b, true, &bb));
+  if (bb == 0.0) {
+    SBX_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * (size_t)N, s));
+    res->converged = 1;
+    return finish(c);
+  }
+  const double bnorm = std::sqrt(bb);
+  double *r, *z, *q, *p;
+  SBX_TRY(work(c, 2, &r));
+  SBX_TRY(work(c, 3, &z));
+  SBX_TRY(work(c, 4, &q));
+  SBX_TRY(work(c, 5, &p));
+  SBX_CUDA(cudaMemcpyAsync(r, b, sizeof(double) * (size_t)N, cudaMemcpyDeviceToDevice, s));
+  // zero-guess test (krylov.cpp:22-28): any x != 0
+  SBX_CUDA(launch_dot_fast(N, x, x, nullptr, c->partials, c->dcount, c->dscal, s));
+  SBX_CUDA(cudaMemcpyAsync(c->hscal, c->dscal, sizeof(double), cudaMemcpyDeviceToHost, s));
+  SBX_TRY(finish(c));
+  // x.x == 0 can underflow for tiny nonzero entries; confirm with an exact scan
+  bool zero_guess = c->hscal[0] == 0.0;
+  if (zero_guess) {
+    std::vector<double> hx(N);
+    SBX_CUDA(cudaMemcpy(hx.data(), x, sizeof(double) * (size_t)N, cudaMemcpyDeviceToHost));
+    for (double v : hx)
+      if (v != 0.0) {
+        zero_guess = false;
+        break;
+      }
+  }
+  if (!zero_guess) {
+    SBX_TRY(apply_dev(c, x, q, cfg->h1, cfg->h2, true, false, true));
+    SBX_CUDA(launch_axpy(N, -1.0, q, r, s));
+  }
+  const bool jacobi = cfg->precond == SBX_PRECOND_JACOBI;
+  if (jacobi) SBX_TRY(ensure_diag(c, cfg->h1, cfg->h2));
+  auto precond = [&](const double* in, double* out) -> sbx_status {
+    if (jacobi)
+      SBX_CUDA(launch_div(N, in, c->ddiag, out, s));
+    else
+      SBX_CUDA(cudaMemcpyAsync(out, in, sizeof(double) * (size_t)N, cudaMemcpyDeviceToDevice, s));
+    return SBX_OK;
+  };
+  SBX_TRY(precond(b, z));
+  double bmb;
+  SBX_TRY(dot_exact(c, b, z, true, &bmb));
+  SBX_TRY(precond(r, z));
+  double rz, rr;
+  SBX_TRY(dot_exact(c, r, z, true, &rz));
+  SBX_TRY(dot_exact(c, r, r, true, &rr));
+  double rnorm = std::sqrt(rr);
+  push(rnorm / bnorm);
+  SBX_CUDA(cudaMemcpyAsync(p, z, sizeof(double) * (size_t)N, cudaMemcpyDeviceToDevice, s));
+  for (int it = 0; it < cfg->max_iterations; ++it) {
+    res->rel_residual = rnorm / bnorm;
+    res->rel_residual_precond = bmb > 0.0 ? std::sqrt(std::max(rz, 0.0) / bmb) : 0.0;
+    if (res->rel_residual <= cfg->tolerance && res->rel_residual_precond <= cfg->tolerance) {
+      res->converged = 1;
+      return finish(c);
+    }
+    SBX_TRY(apply_dev(c, p, q, cfg->h1, cfg->h2, true, false, true));
+    double pq;
+    SBX_TRY(dot_exact(c, p, q, true, &pq));
+    if (!std::isfinite(pq) || pq <= 0.0) {
+      res->error_iteration = it;
+      set_error("pcg: breakdown (p'Ap = " + std::to_string(pq) + ") at iteration " +
+                std::to_string(it));
+      return SBX_E_BREAKDOWN;
+    }
+    const double alpha = rz / pq;
+    SBX_CUDA(launch_axpy(N, alpha, p, x, s));
+    SBX_CUDA(launch_axpy(N, -alpha, q, r, s));
+    SBX_TRY(precond(r, z));
+    double rz_new;
+    SBX_TRY(dot_exact(c, r, z, true, &rz_new));
+    SBX_TRY(dot_exact(c, r, r, true, &rr));
+    rnorm = std::sqrt(rr);
+    if (!std::isfinite(rnorm) || !std::isfinite(rz_new)) {
+      res->error_iteration = it;
+      set_error("pcg: residual diverged (NaN/Inf) at iteration " + std::to_string(it));
+      return SBX_E_NAN;
+    }
+    push(rnorm / bnorm);
+    ++res->iterations;
+    const double beta = rz_new / rz;
+    rz = rz_new;
+    SBX_CUDA(launch_scale(N, beta, p, s));
+    SBX_CUDA(launch_axpy(N, 1.0, z, p, s));
+  }
+  res->rel_residual = rnorm / bnorm;
+  res->rel_residual_precond = bmb > 0.0 ? std::sqrt(std::max(rz, 0.0) / bmb) : 0.0;
+  res->converged = res->rel_residual <= cfg->tolerance &&
+                   res->rel_residual_precond <= cfg->tolerance;
+  return finish(c);
+}
+
+}  // namespace
+
+// =========================================================================
+extern "C" {
+
+const char* sbx_last_error(void) { return g_last_error.c_str(); }
+const char* sbx_version(void) { return "sbx 0.1 (sm_100a)"; }
+
+sbx_status sbx_gll_basis(int degree, double* nodes, double* weights, double* deriv) {
+  const int rc = gll_basis(degree, nodes, weights, deriv);
+  if (rc) set_error("build_gll_basis: degree must be in [1,32], got " + std::to_string(degree));
+  return (sbx_status)rc;
+}
+
+sbx_status sbx_box_corners(int ex, int ey, int ez, const double origin[3],
+                           const double lengths[3], double* corners) {
+  const int rc = box_corners(ex, ey, ez, origin, lengths, corners);
+  if (rc) set_error("build_box_mesh: element counts must be >= 1 and extents positive");
+  return (sbx_status)rc;
+}
+
+sbx_status sbx_deform_corners(int64_t elem_count, double amplitude, double* corners) {
+  deform_corners(elem_count, amplitude, corners);
+  return SBX_OK;
+}
+
+sbx_status sbx_geometric_factors(int64_t elem_count, int degree, const double* corners,
+                                 double* g1, double* g2, double* g3, double* g4, double* g5,
+                                 double* g6, double* bm, double* jac, int64_t* bad_elem) {
+  double* const g[6] = {g1, g2, g3, g4, g5, g6};
+  int64_t bad = -1;
+  const int rc = geometric_factors(elem_count, degree, corners, g, bm, jac, &bad);
+  if (bad_elem) *bad_elem = bad;
+  if (rc == SBX_E_MESH)
+    set_error("build_geometric_factors: nonpositive Jacobian in element " + std::to_string(bad));
+  else if (rc)
+    set_error("build_geometric_factors: bad degree");
+  return (sbx_status)rc;
+}
+
+sbx_status sbx_gather_scatter(int ex, int ey, int ez, const int periodic[3], int degree,
+                              int64_t* gid, int64_t* group_offsets, int64_t* group_nodes,
+                              int32_t* mult, double* inv_mult, int64_t* global_count) {
+  const int rc = gather_scatter(ex, ey, ez, periodic, degree, gid, group_offsets, group_nodes,
+                                mult, inv_mult, global_count);
+  if (rc) set_error("build_gather_scatter: degree must be >= 1");
+  return (sbx_status)rc;
+}
+
+sbx_status sbx_dirichlet_mask(int ex, int ey, int ez, const int periodic[3], int degree,
+                              double* mask) {
+  return (sbx_status)dirichlet_mask(ex, ey, ez, periodic, degree, mask);
+}
+
+sbx_status sbx_partition_rcb(int64_t elem_count, const double* corners, int ranks,
+                             int32_t* rank_of) {
+  const int rc = partition_rcb(elem_count, corners, ranks, rank_of);
+  if (rc)
+    set_error("partition_rcb: ranks (" + std::to_string(ranks) + ") must be in [1, " +
+              std::to_string(elem_count) + "]");
+  return (sbx_status)rc;
+}
+
+sbx_status sbx_ctx_create(const sbx_problem_desc* desc, int device, sbx_ctx** out) {
+  if (!desc || !out || !desc->deriv || !desc->group_offsets || !desc->group_nodes) {
+    set_error("sbx_ctx_create: null argument");
+    return SBX_E_INVALID;
+  }
+  for (int q = 0; q < 6; ++q)
+    if (!desc->g[q]) {
+      set_error("sbx_ctx_create: null geometric factor");
+      return SBX_E_INVALID;
+    }
+  if (desc->degree < 1 || desc->degree > kMaxDegree) {
+    set_error("sbx_ctx_create: degree must be in [1,32]");
+    return SBX_E_CONFIG;
+  }
+  if (desc->elem_count < 1) {
+    set_error("sbx_ctx_create: elem_count must be >= 1");
+    return SBX_E_SHAPE;
+  }
+  *out = nullptr;
+  auto* c = new sbx_ctx();
+  sbx_status st = ctx_init_common(c, device);
+  if (st == SBX_OK) st = ctx_upload(c, desc);
+  if (st != SBX_OK) {
+    sbx_ctx_destroy(c);
+    return st;
+  }
+  *out = c;
+  return SBX_OK;
+}
+
+sbx_status sbx_ctx_create_box(const sbx_box_desc* d, int device, sbx_ctx** out) {
+  if (!d || !out) {
+    set_error("sbx_ctx_create_box: null argument");
+    return SBX_E_INVALID;
+  }
+  if (d->degree < 1 || d->degree > kMaxDegree) {
+    set_error("build_gll_basis: degree must be in [1,32], got " + std::to_string(d->degree));
+    return SBX_E_CONFIG;
+  }
+  const int64_t E = (int64_t)d->ex * d->ey * d->ez;
+  const int n = d->degree + 1;
+  const int64_t N = E * n * n * n;
+  std::vector<double> corners(E * 24);
+  SBX_TRY(sbx_box_corners(d->ex, d->ey, d->ez, d->origin, d->lengths, corners.data()));
+  if (d->deform_amplitude != 0.0) deform_corners(E, d->deform_amplitude, corners.data());
+  std::vector<double> deriv(n * n);
+  SBX_TRY(sbx_gll_basis(d->degree, nullptr, nullptr, deriv.data()));
+  std::vector<std::vector<double>> g(7, std::vector<double>(N));
+  int64_t bad = -1;
+  SBX_TRY(sbx_geometric_factors(E, d->degree, corners.data(), g[0].data(), g[1].data(),
+                                g[2].data(), g[3].data(), g[4].data(), g[5].data(), g[6].data(),
+                                nullptr, &bad));
+  corners.clear();
+  corners.shrink_to_fit();
+  std::vector<int64_t> offsets(N + 1), nodes(N);
+  int64_t G = 0;
+  SBX_TRY(sbx_gather_scatter(d->ex, d->ey, d->ez, d->periodic, d->degree, nullptr,
+                             offsets.data(), nodes.data(), nullptr, nullptr, &G));
+  std::vector<double> mask(N);
+  SBX_TRY(sbx_dirichlet_mask(d->ex, d->ey, d->ez, d->periodic, d->degree, mask.data()));
+  sbx_problem_desc pd{};
+  pd.elem_count = E;
+  pd.degree = d->degree;
+  pd.deriv = deriv.data();
+  for (int q = 0; q < 6; ++q) pd.g[q] = g[q].data();
+  pd.bm = g[6].data();
+  pd.mask = mask.data();
+  pd.global_count = G;
+  pd.group_offsets = offsets.data();
+  pd.group_nodes = nodes.data();
+  return sbx_ctx_create(&pd, device, out);
+}
+
+void sbx_ctx_destroy(sbx_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  c->cg.reset();
+  for (void* p : c->allocs) cudaFree(p);
+  if (c->hscal) cudaFreeHost(c->hscal);
+  if (c->own_stream) cudaStreamDestroy(c->own_stream);
+  delete c;
+}
+
+sbx_status sbx_ctx_info(const sbx_ctx* c, int64_t* E, int32_t* n1d, int64_t* nodes,
+                        int64_t* G, int64_t* bytes) {
+  SBX_TRY(check_ctx(c));
+  if (E) *E = c->op.E;
+  if (n1d) *n1d = c->op.n;
+  if (nodes) *nodes = c->op.nodes;
+  if (G) *G = c->global_count;
+  if (bytes) *bytes = c->device_bytes;
+  return SBX_OK;
+}
+
+sbx_status sbx_ctx_set_stream(sbx_ctx* c, void* stream) {
+  SBX_TRY(check_ctx(c));
+  c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
+  return SBX_OK;
+}
+
+sbx_status sbx_ctx_copy_array(const sbx_ctx* c, int which, double* out) {
+  SBX_TRY(check_ctx(c));
+  const int64_t N = c->op.nodes;
+  const int n3 = c->op.n * c->op.n * c->op.n;
+  cudaSetDevice(c->device);
+  auto copy = [&](const double* src, int64_t count) -> sbx_status {
+    if (!src) {
+      set_error("sbx_ctx_copy_array: array not present");
+      return SBX_E_INVALID;
+    }
+    SBX_CUDA(cudaMemcpy(out, src, sizeof(double) * (size_t)count, cudaMemcpyDefault));
+    return SBX_OK;
+  };
+  switch (which) {
+    case 0: return copy(c->op.mask, N);
+    case 1: return copy(c->op.inv_mult, N);
+    case 2: return copy(c->op.bm, N);
+    case 9: return copy(c->op.Dd, (int64_t)c->op.n * c->op.n);
+    default:
+      if (which >= 3 && which <= 8) {
+        std::vector<double> G(6 * N);
+        SBX_CUDA(cudaMemcpy(G.data(), c->op.G, sizeof(double) * 6 * (size_t)N,
+                            cudaMemcpyDeviceToHost));
+        std::vector<double> h(N);
+        const int comp = which - 3;
+        for (int64_t e = 0; e < c->op.E; ++e)
+          std::memcpy(&h[e * n3], &G[(e * 6 + comp) * n3], sizeof(double) * n3);
+        SBX_CUDA(cudaMemcpy(out, h.data(), sizeof(double) * (size_t)N, cudaMemcpyDefault));
+        return SBX_OK;
+      }
+      set_error("sbx_ctx_copy_array: unknown array id");
+      return SBX_E_INVALID;
+  }
+}
+
+sbx_status sbx_axhelm(sbx_ctx* c, const double* u, double* w, double h1, double h2,
+                      uint32_t flags) {
+  SBX_TRY(check_ctx(c));
+  if (!u || !w) {
+    set_error("sbx_axhelm: null field");
+    return SBX_E_INVALID;
+  }
+  if (h2 != 0.0 && !c->op.bm) {
+    set_error("axhelm: h2 != 0 needs the mass factors (bm)");
+    return SBX_E_SHAPE;
+  }
+  SBX_CUDA(cudaSetDevice(c->device));
+  const double* du = nullptr;
+  SBX_TRY(stage_in(c, u, 0, &du));
+  const bool wdev = is_device_ptr(w);
+  double* dw = w;
+  if (!wdev) SBX_TRY(work(c, 1, &dw));
+  SBX_CUDA(launch_axhelm(c->op, du, dw, h1, h2, flags & SBX_FLAG_EXACT,
+                         flags & SBX_FLAG_FLIP_T, c->stream));
+  if (!wdev)
+    SBX_CUDA(cudaMemcpyAsync(w, dw, sizeof(double) * (size_t)c->op.nodes, cudaMemcpyDeviceToHost,
+                             c->stream));
+  return finish(c);
+}
+
+sbx_status sbx_axhelm_diagonal(sbx_ctx* c, double h1, double h2, int assembled, double* diag) {
+  SBX_TRY(check_ctx(c));
+  if (!diag) {
+    set_error("sbx_axhelm_diagonal: null output");
+    return SBX_E_INVALID;
+  }
+  SBX_CUDA(cudaSetDevice(c->device));
+  const bool ddev = is_device_ptr(diag);
+  double* dd = diag;
+  if (!ddev) SBX_TRY(work(c, 1, &dd));
+  SBX_CUDA(launch_axhelm_diag(c->op, h1, h2, dd, c->stream));
+  if (assembled) SBX_CUDA(launch_gs(c->op, dd, false, c->stream));
+  if (!ddev)
+    SBX_CUDA(cudaMemcpyAsync(diag, dd, sizeof(double) * (size_t)c->op.nodes,
+                             cudaMemcpyDeviceToHost, c->stream));
+  return finish(c);
+}
+
+sbx_status sbx_gs_sum(sbx_ctx* c, double* f) {
+  SBX_TRY(check_ctx(c));
+  if (!f) {
+    set_error("sbx_gs_sum: null field");
+    return SBX_E_INVALID;
+  }
+  SBX_CUDA(cudaSetDevice(c->device));
+  const bool dev = is_device_ptr(f);
+  double* df = f;
+  if (!dev) {
+    SBX_TRY(work(c, 1, &df));
+    SBX_CUDA(cudaMemcpyAsync(df, f, sizeof(double) * (size_t)c->op.nodes,
+                             cudaMemcpyHostToDevice, c->stream));
+  }
+  SBX_CUDA(launch_gs(c->op, df, false, c->stream));
+  if (!dev)
+    SBX_CUDA(cudaMemcpyAsync(f, df, sizeof(double) * (size_t)c->op.nodes, cudaMemcpyDeviceToHost,
+                             c->stream));
+  return finish(c);
+}
+
+sbx_status sbx_apply(sbx_ctx* c, const double* x, double* q, double h1, double h2,
+                     uint32_t flags) {
+  SBX_TRY(check_ctx(c));
+  if (!x || !q) {
+    set_error("sbx_apply: null field");
+    return SBX_E_INVALID;
+  }
+  if (h2 != 0.0 && !c->op.bm) {
+    set_error("apply: h2 != 0 needs the mass factors (bm)");
+    return SBX_E_SHAPE;
+  }
+  SBX_CUDA(cudaSetDevice(c->device));
+  const double* dx = nullptr;
+  SBX_TRY(stage_in(c, x, 0, &dx));
+  const bool qdev = is_device_ptr(q);
+  double* dq = q;
+  if (!qdev) SBX_TRY(work(c, 1, &dq));
+  SBX_TRY(apply_dev(c, dx, dq, h1, h2, flags & SBX_FLAG_EXACT, flags & SBX_FLAG_FLIP_T,
+                    !(flags & SBX_FLAG_NO_MASK)));
+  if (!qdev)
+    SBX_CUDA(cudaMemcpyAsync(q, dq, sizeof(double) * (size_t)c->op.nodes, cudaMemcpyDeviceToHost,
+                             c->stream));
+  return finish(c);
+}
+
+sbx_status sbx_dot(sbx_ctx* c, const double* a, const double* b, int weighted, uint32_t flags,
+                   double* result) {
+  SBX_TRY(check_ctx(c));
+  if (!a || !b || !result) {
+    set_error("sbx_dot: null argument");
+    return SBX_E_INVALID;
+  }
+  SBX_CUDA(cudaSetDevice(c->device));
+  const double *da = nullptr, *db = nullptr;
+  SBX_TRY(stage_in(c, a, 0, &da));
+  SBX_TRY(stage_in(c, b, 1, &db));
+  if (flags & SBX_FLAG_EXACT) return dot_exact(c, da, db, weighted != 0, result);
+  SBX_CUDA(launch_dot_fast(c->op.nodes, da, db, weighted ? c->op.inv_mult : nullptr,
+                           c->partials, c->dcount, c->dscal, c->stream));
+  SBX_CUDA(cudaMemcpyAsync(c->hscal, c->dscal, sizeof(double), cudaMemcpyDeviceToHost,
+                           c->stream));
+  SBX_TRY(finish(c));
+  *result = c->hscal[0];
+  return SBX_OK;
+}
+
+void sbx_pcg_config_default(sbx_pcg_config* cfg) {
+  std::memset(cfg, 0, sizeof(*cfg));
+  cfg->tolerance = 1e-8;
+  cfg->max_iterations = 500;
+  cfg->precond = SBX_PRECOND_JACOBI;
+  cfg->mode = SBX_MODE_FAST;
+  cfg->h1 = 1.0;
+  cfg->h2 = 0.0;
+}
+
+sbx_status sbx_pcg(sbx_ctx* c, const double* b, double* x, const sbx_pcg_config* cfg,
+                   sbx_pcg_result* res) {
+  SBX_TRY(check_ctx(c));
+  if (!b || !x || !cfg || !res) {
+    set_error("sbx_pcg: null argument");
+    return SBX_E_INVALID;
+  }
+  if (cfg->h2 != 0.0 && !c->op.bm) {
+    set_error("pcg: h2 != 0 needs the mass factors (bm)");
+    return SBX_E_SHAPE;
+  }
+  SBX_CUDA(cudaSetDevice(c->device));
+  std::memset(res, 0, sizeof(*res));
+  res->error_iteration = -1;
+  const int64_t N = c->op.nodes;
+  const double* db = nullptr;
+  SBX_TRY(stage_in(c, b, 0, &db));
+  const bool xdev = is_device_ptr(x);
+  double* dx = x;
+  if (!xdev) {
+    SBX_TRY(work(c, 1, &dx));
+    SBX_CUDA(cudaMemcpyAsync(dx, x, sizeof(double) * (size_t)N, cudaMemcpyHostToDevice,
+                             c->stream));
+  }
+  sbx_status st;
+  if (cfg->mode == SBX_MODE_FAST) {
+    if (cfg->precond == SBX_PRECOND_JACOBI) SBX_TRY(ensure_diag(c, cfg->h1, cfg->h2));
+    CgRun run;
+    run.op = &c->op;
+    run.stream = c->stream;
+    run.b = db;
+    run.x = dx;
+    run.dinv = cfg->precond == SBX_PRECOND_JACOBI ? c->ddinv : nullptr;
+    run.h1 = cfg->h1;
+    run.h2 = cfg->h2;
+    run.tol = cfg->tolerance;
+    run.max_it = cfg->max_iterations;
+    run.history = cfg->history;
+    run.history_capacity = cfg->history_capacity;
+    run.interior_clean = c->interior_clean;
+    run.timing = c->timing;
+    const int rc = c->cg->solve(run, res);
+    st = (sbx_status)rc;
+    if (rc == kCgFallback) {
+      // FAST schedule preconditions not met (see cg.cu): reference-order path
+      std::memset(res, 0, sizeof(*res));
+      res->error_iteration = -1;
+      st = pcg_exact(c, db, dx, cfg, res);
+    } else if (st == SBX_E_CUDA) set_error(c->cg->error());
+    else if (st == SBX_E_BREAKDOWN)
+      set_error("pcg: breakdown (p'Ap <= 0 or non-finite) at iteration " +
+                std::to_string(res->error_iteration));
+    else if (st == SBX_E_NAN)
+      set_error("pcg: residual diverged (NaN/Inf) at iteration " +
+                std::to_string(res->error_iteration));
+    else if (st == SBX_E_SHAPE) set_error(c->cg->error());
+  } else {
+    st = pcg_exact(c, db, dx, cfg, res);
+  }
+  if (!xdev && (st == SBX_OK || st == SBX_E_BREAKDOWN || st == SBX_E_NAN)) {
+    SBX_CUDA(cudaMemcpyAsync(x, dx, sizeof(double) * (size_t)N, cudaMemcpyDeviceToHost,
+                             c->stream));
+    sbx_status f = finish(c);
+    if (st == SBX_OK) st = f;
+  }
+  return st;
+}
+
+sbx_status sbx_ctx_enable_timing(sbx_ctx* c, int enable) {
+  SBX_TRY(check_ctx(c));
+  c->timing = enable != 0;
+  return SBX_OK;
+}
+
+sbx_status sbx_ctx_kernel_time(const sbx_ctx* c, const char* name, double* total_ms,
+                               int64_t* launches) {
+  SBX_TRY(check_ctx(c));
+  if (!c->cg) return SBX_E_INVALID;
+  return (sbx_status)c->cg->kernel_time(name, total_ms, launches);
+}
+
+sbx_status sbx_ctx_local_elements(const sbx_ctx* c, int64_t* ids) {
+  SBX_TRY(check_ctx(c));
+  if (c->local_elements.empty()) {
+    for (int64_t e = 0; e < c->op.E; ++e) ids[e] = e;
+  } else {
+    std::memcpy(ids, c->local_elements.data(), sizeof(int64_t) * c->local_elements.size());
+  }
+  return SBX_OK;
+}
+
+}  // extern "C"
+
+// ---- multi-GPU entry points: see dist.cu -----------------------------------

@@ -1,0 +1,643 @@
+// FAST PCG (krylov.cpp:7-91 semantics, fused schedule) for sm_100a.
+//
+// Per iteration two kernels:
+//   K1 cg_ax_kernel     : z = r/diag (as r*dinv), p = z + beta*p_old,
+//                         x += alpha_prev*p_old, w = axhelm(p), and the
+//                         block partials of p'Ap = sum_local p.w (valid because
+//                         p is continuous and masked, so p'(mask*QQ^T w)/mult
+//                         == p.w summed over local nodes); the last CTA
+//                         computes alpha = rz/pq and the breakdown test.
+//   K2 cg_update_kernel : gather-scatter + mask on the boundary groups fused
+//                         with r -= alpha*q, z = r*dinv and the weighted dots
+//                         r'z, r'r; element-interior nodes (q = w) in the same
+//                         launch; the last CTA computes beta, appends the
+//                         residual history, tests convergence (both relative
+//                         residuals <= tol, krylov.cpp:51-57) and NaN/Inf
+//                         (krylov.cpp:72-75), and sets the graph's WHILE
+//                         condition.
+// Reductions are deterministic (fixed block partials, fixed-order final sum).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "ax_core.cuh"
+#include "cg.cuh"
+#include "sbx_internal.h"
+
+namespace sbx {
+
+namespace {
+
+constexpr int kUpdThreads = 256;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Sum over the CTA; result valid in thread 0.  sh: >= 32 doubles.
+__device__ __forceinline__ double cta_sum(double v, double* sh) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  const int nw = (blockDim.x + 31) >> 5;
+  v = (int)threadIdx.x < nw ? sh[threadIdx.x] : 0.0;
+  if (wid == 0) v = warp_sum(v);
+  return v;
+}
+
+// Last-block ticket: returns true in every thread of the CTA that arrived last.
+__device__ __forceinline__ bool last_block(uint32_t* counter, bool* sflag) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const uint32_t t = atomicAdd(counter, 1u);
+    *sflag = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (*sflag) __threadfence();
+  return *sflag;
+}
+
+// Fixed-order sum of partials[0..count) * stride + off, by one CTA.
+__device__ double reduce_partials(const double* partials, int count, int stride, int off,
+                                  double* sh) {
+  double s = 0.0;
+  for (int q = threadIdx.x; q < count; q += blockDim.x) s += partials[(int64_t)q * stride + off];
+  return cta_sum(s, sh);
+}
+
+// ---------------------------------------------------------------- K1 -----
+template <int n>
+__global__ void __launch_bounds__(AxCfg<n>::threads)
+    cg_ax_kernel(const double* __restrict__ r, const double* __restrict__ dinv,
+                 double* __restrict__ p, double* __restrict__ x, double* __restrict__ w,
+                 const double* __restrict__ G, const double* __restrict__ bm, int64_t E,
+                 double h1, double h2, DParam<n> Dp, CgScalars* __restrict__ sc,
+                 double* __restrict__ partials) {
+  using C = AxCfg<n>;
+  if (sc->done) return;
+  extern __shared__ double sm[];
+  __shared__ double red[32];
+  __shared__ bool is_last;
+  double* sD = sm;
+  const int t = threadIdx.x;
+  const int slot = t / C::nn, ij = t % C::nn, i = ij % n, j = ij / n;
+  double* su = sm + n * C::DS + slot * 3 * C::TILE;
+  ax_stage_D<n>(sD, Dp);
+  const int64_t e = (int64_t)blockIdx.x * C::EPB + slot;
+  const bool valid = e < E;
+  const int64_t base = e * C::n3 + ij;
+  const bool first = sc->first != 0;
+  const double beta = sc->beta, ap = sc->alpha_prev;
+  double uc[n];
+#pragma unroll
+  for (int k = 0; k < n; ++k) {
+    double pv = 0.0;
+    if (valid) {
+      const int64_t a = base + k * C::nn;
+      const double rv = r[a];
+      const double z = dinv ? rv * __ldg(dinv + a) : rv;
+      if (first) {
+        pv = z;
+      } else {
+        const double po = p[a];
+        pv = fma(beta, po, z);
+        x[a] = fma(ap, po, x[a]);
+      }
+      p[a] = pv;
+    }
+    uc[k] = pv;
+    su[k * C::SP + j * C::SR + i] = pv;
+  }
+  double acc[n];
+  ax_column<n, false>(uc, su, su + C::TILE, su + 2 * C::TILE, sD,
+                      G + (valid ? e : 0) * 6 * C::n3 + ij, valid, i, j, h1, 1.0, Dp, acc);
+  double pq = 0.0;
+  if (valid) {
+#pragma unroll
+    for (int k = 0; k < n; ++k) {
+      const int64_t a = base + k * C::nn;
+      const double out = bm ? fma(h2 * __ldg(bm + a), uc[k], acc[k]) : acc[k];
+      w[a] = out;
+      pq = fma(uc[k], out, pq);
+    }
+  }
+  pq = cta_sum(pq, red);
+  if (t == 0) partials[blockIdx.x] = pq;
+  if (!last_block(&sc->counter[0], &is_last)) return;
+  const double tot = reduce_partials(partials, gridDim.x, 1, 0, red);
+  if (t == 0) {
+    sc->counter[0] = 0;
+    sc->pq = tot;
+    if (!isfinite(tot) || tot <= 0.0) {
+      sc->status = 5;
+      sc->err_it = sc->it;
+      sc->done = 1;
+    } else {
+      sc->alpha = sc->rz / tot;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- K2 -----
+__device__ __forceinline__ void upd_node(double* __restrict__ r, const double* __restrict__ dinv,
+                                         int64_t a, double q, double alpha, double wgt,
+                                         double& rz, double& rr) {
+  const double rv = fma(-alpha, q, r[a]);
+  r[a] = rv;
+  const double z = dinv ? rv * __ldg(dinv + a) : rv;
+  rz = fma(rv * z, wgt, rz);
+  rr = fma(rv * rv, wgt, rr);
+}
+
+template <int n>
+__global__ void __launch_bounds__(kUpdThreads)
+    cg_update_kernel(const int32_t* __restrict__ b_off, const int32_t* __restrict__ b_idx,
+                     int64_t nB, int64_t nBblocks, int64_t E, const double* __restrict__ w,
+                     double* __restrict__ r, const double* __restrict__ dinv,
+                     CgScalars* __restrict__ sc, double* __restrict__ partials,
+                     double* __restrict__ hist, int64_t hist_cap,
+                     cudaGraphConditionalHandle cond, int use_cond) {
+  __shared__ double red[32];
+  __shared__ bool is_last;
+  if (sc->done) {
+    if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0);
+    return;
+  }
+  const double alpha = sc->alpha;
+  double rz = 0.0, rr = 0.0;
+  if ((int64_t)blockIdx.x < nBblocks) {
+    const int64_t g = (int64_t)blockIdx.x * kUpdThreads + threadIdx.x;
+    if (g < nB) {
+      const int lo = b_off[g], hi = b_off[g + 1];
+      const int m = hi - lo;
+      const double wgt = 1.0 / (double)m;
+      double s = 0.0;
+      if (m == 1) {
+        const int32_t c = b_idx[lo];
+        s = w[c < 0 ? ~c : c];
+      } else {
+        for (int c = lo; c < hi; ++c) {
+          const int32_t a = b_idx[c];
+          s += w[a < 0 ? ~a : a];
+        }
+      }
+      for (int c = lo; c < hi; ++c) {
+        const int32_t a = b_idx[c];
+        if (a >= 0)
+          upd_node(r, dinv, a, s, alpha, wgt, rz, rr);
+        else
+          upd_node(r, dinv, ~a, 0.0, alpha, wgt, rz, rr);
+      }
+    }
+  } else {
+    constexpr int m = n - 2;
+    constexpr int m3 = m * m * m;
+    if constexpr (m > 0) {
+      const int64_t q = ((int64_t)blockIdx.x - nBblocks) * kUpdThreads + threadIdx.x;
+      if (q < E * m3) {
+        const int64_t e = q / m3;
+        const int l = (int)(q - e * m3);
+        const int ii = l % m + 1, jj = (l / m) % m + 1, kk = l / (m * m) + 1;
+        const int64_t a = e * (n * n * n) + (kk * n + jj) * n + ii;
+        upd_node(r, dinv, a, w[a], alpha, 1.0, rz, rr);
+      }
+    }
+  }
+  rz = cta_sum(rz, red);
+  const double rz_b = rz;
+  rr = cta_sum(rr, red);
+  if (threadIdx.x == 0) {
+    partials[2 * (int64_t)blockIdx.x] = rz_b;
+    partials[2 * (int64_t)blockIdx.x + 1] = rr;
+  }
+  if (!last_block(&sc->counter[1], &is_last)) return;
+  const double rz_new = reduce_partials(partials, gridDim.x, 2, 0, red);
+  const double rr_new = reduce_partials(partials, gridDim.x, 2, 1, red);
+  if (threadIdx.x == 0) {
+    sc->counter[1] = 0;
+    const double rnorm = sqrt(rr_new);
+    const int it = sc->it;
+    if (!isfinite(rnorm) || !isfinite(rz_new)) {
+      sc->status = 6;
+      sc->err_it = it;
+      sc->done = 1;
+    } else {
+      const double rel = rnorm / sc->bnorm;
+      if (hist && it + 1 < hist_cap) hist[it + 1] = rel;
+      sc->it = it + 1;
+      sc->beta = rz_new / sc->rz;
+      sc->rz = rz_new;
+      sc->rr = rr_new;
+      sc->alpha_prev = alpha;
+      sc->first = 0;
+      sc->rel = rel;
+      sc->relp = sc->bmb > 0.0 ? sqrt(fmax(rz_new, 0.0) / sc->bmb) : 0.0;
+      if (sc->rel <= sc->tol && sc->relp <= sc->tol) {
+        sc->converged = 1;
+        sc->done = 1;
+      } else if (sc->it >= sc->max_it) {
+        sc->done = 1;
+      }
+    }
+    if (use_cond) cudaGraphSetConditional(cond, sc->done ? 0 : 1);
+  }
+}
+
+// x += alpha*p for the last completed iteration (K1 of the next iteration
+// would have done it).
+__global__ void cg_finish_kernel(int64_t N, const double* __restrict__ p, double* __restrict__ x,
+                                 const CgScalars* __restrict__ sc) {
+  if (sc->first || sc->status == 5) return;
+  const double a = sc->alpha;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < N;
+       q += (int64_t)gridDim.x * blockDim.x)
+    x[q] = fma(a, p[q], x[q]);
+}
+
+// Init sums: [b'Wb, b'W(M b), r'W(M r), r'Wr] and r = b - q (q may be null).
+__global__ void cg_init_kernel(int64_t N, const double* __restrict__ b,
+                               const double* __restrict__ q, const double* __restrict__ dinv,
+                               const double* __restrict__ wgt, double* __restrict__ r,
+                               double* __restrict__ partials, uint32_t* counter,
+                               double* __restrict__ out) {
+  __shared__ double red[32];
+  __shared__ bool is_last;
+  double s[4] = {0, 0, 0, 0};
+  for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < N;
+       a += (int64_t)gridDim.x * blockDim.x) {
+    const double bv = b[a], wv = wgt[a];
+    const double rv = q ? bv - q[a] : bv;
+    r[a] = rv;
+    const double di = dinv ? dinv[a] : 1.0;
+    s[0] += bv * bv * wv;
+    s[1] += bv * (bv * di) * wv;
+    s[2] += rv * (rv * di) * wv;
+    s[3] += rv * rv * wv;
+  }
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const double v = cta_sum(s[c], red);
+    if (threadIdx.x == 0) partials[4 * (int64_t)blockIdx.x + c] = v;
+  }
+  if (!last_block(counter, &is_last)) return;
+  for (int c = 0; c < 4; ++c) {
+    const double v = reduce_partials(partials, gridDim.x, 4, c, red);
+    if (threadIdx.x == 0) out[c] = v;
+  }
+  if (threadIdx.x == 0) *counter = 0;
+}
+
+// Continuity + mask check of the right-hand side on the boundary groups: the
+// fused p'Ap identity needs b (hence r, z, p) equal on all copies and zero
+// on masked copies.  flag := 1 on violation.
+__global__ void cg_check_rhs_kernel(const int32_t* __restrict__ b_off,
+                                    const int32_t* __restrict__ b_idx, int64_t nB,
+                                    const double* __restrict__ b, int* flag) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= nB) return;
+  const int lo = b_off[g], hi = b_off[g + 1];
+  const int32_t a0 = b_idx[lo];
+  const double v0 = b[a0 < 0 ? ~a0 : a0];
+  for (int c = lo; c < hi; ++c) {
+    const int32_t a = b_idx[c];
+    const double v = b[a < 0 ? ~a : a];
+    if (v != v0 || (a < 0 && v != 0.0)) *flag = 1;
+  }
+}
+
+template <int n>
+cudaError_t launch_k1(const OpDev& op, const double* r, const double* dinv, double* p, double* x,
+                      double* w, double h1, double h2, CgScalars* sc, double* partials,
+                      cudaStream_t s) {
+  using C = AxCfg<n>;
+  static bool attr_set[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!attr_set[dev & 63]) {
+    cudaError_t err = cudaFuncSetAttribute(
+        cg_ax_kernel<n>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem);
+    if (err != cudaSuccess) return err;
+    attr_set[dev & 63] = true;
+  }
+  DParam<n> Dp;
+  for (int q = 0; q < n * n; ++q) Dp.d[q] = op.Dh[q];
+  const int64_t blocks = (op.E + C::EPB - 1) / C::EPB;
+  cg_ax_kernel<n><<<(unsigned)blocks, C::threads, C::smem, s>>>(
+      r, dinv, p, x, w, op.G, h2 != 0.0 ? op.bm : nullptr, op.E, h1, h2, Dp, sc, partials);
+  return cudaGetLastError();
+}
+
+template <int n>
+cudaError_t launch_k2(const OpDev& op, const double* w, double* r, const double* dinv,
+                      CgScalars* sc, double* partials, double* hist, int64_t hist_cap,
+                      cudaGraphConditionalHandle cond, int use_cond, cudaStream_t s) {
+  const int64_t nBblocks = (op.nB + kUpdThreads - 1) / kUpdThreads;
+  const int64_t m = n - 2;
+  const int64_t nI = m > 0 ? op.E * m * m * m : 0;
+  const int64_t nIblocks = (nI + kUpdThreads - 1) / kUpdThreads;
+  int64_t blocks = nBblocks + nIblocks;
+  if (blocks < 1) blocks = 1;
+  cg_update_kernel<n><<<(unsigned)blocks, kUpdThreads, 0, s>>>(
+      op.b_off, op.b_idx, op.nB, nBblocks, op.E, w, r, dinv, sc, partials, hist, hist_cap, cond,
+      use_cond);
+  return cudaGetLastError();
+}
+
+int64_t k1_blocks(const OpDev& op) {
+  int epb = 256 / (op.n * op.n);
+  if (epb < 1) epb = 1;
+  return (op.E + epb - 1) / epb;
+}
+int64_t k2_blocks(const OpDev& op) {
+  const int64_t m = op.n - 2;
+  const int64_t nI = m > 0 ? op.E * m * m * m : 0;
+  return (op.nB + kUpdThreads - 1) / kUpdThreads + (nI + kUpdThreads - 1) / kUpdThreads + 1;
+}
+
+#define SBX_N_SWITCH(NVAL, CALL)                                               \
+  switch (NVAL) {                                                              \
+    case 2: CALL(2); break;                                                    \
+    case 3: CALL(3); break;                                                    \
+    case 4: CALL(4); break;                                                    \
+    case 5: CALL(5); break;                                                    \
+    case 6: CALL(6); break;                                                    \
+    case 7: CALL(7); break;                                                    \
+    case 8: CALL(8); break;                                                    \
+    case 9: CALL(9); break;                                                    \
+    case 10: CALL(10); break;                                                  \
+    case 11: CALL(11); break;                                                  \
+    case 12: CALL(12); break;                                                  \
+    case 13: CALL(13); break;                                                  \
+    case 14: CALL(14); break;                                                  \
+    case 15: CALL(15); break;                                                  \
+    case 16: CALL(16); break;                                                  \
+    default: err = cudaErrorInvalidValue;                                      \
+  }
+
+cudaError_t k1(const OpDev& op, const double* r, const double* dinv, double* p, double* x,
+               double* w, double h1, double h2, CgScalars* sc, double* partials,
+               cudaStream_t s) {
+  cudaError_t err = cudaSuccess;
+#define CALL1(NN) err = launch_k1<NN>(op, r, dinv, p, x, w, h1, h2, sc, partials, s)
+  SBX_N_SWITCH(op.n, CALL1)
+#undef CALL1
+  return err;
+}
+
+cudaError_t k2(const OpDev& op, const double* w, double* r, const double* dinv, CgScalars* sc,
+               double* partials, double* hist, int64_t hist_cap, cudaGraphConditionalHandle cond,
+               int use_cond, cudaStream_t s) {
+  cudaError_t err = cudaSuccess;
+#define CALL2(NN) \
+  err = launch_k2<NN>(op, w, r, dinv, sc, partials, hist, hist_cap, cond, use_cond, s)
+  SBX_N_SWITCH(op.n, CALL2)
+#undef CALL2
+  return err;
+}
+
+}  // namespace
+
+#define CG_CUDA(call)                                                       \
+  do {                                                                      \
+    cudaError_t _e = (call);                                                \
+    if (_e != cudaSuccess) {                                                \
+      err_ = std::string(#call) + ": " + cudaGetErrorString(_e);            \
+      return SBX_E_CUDA;                                                    \
+    }                                                                       \
+  } while (0)
+
+CgEngine::~CgEngine() {
+  if (exec_) cudaGraphExecDestroy(exec_);
+  if (graph_) cudaGraphDestroy(graph_);
+  cudaFree(r_);
+  cudaFree(p_);
+  cudaFree(w_);
+  cudaFree(partials_);
+  cudaFree(sc_);
+  cudaFree(hist_);
+  cudaFree(init_);
+  cudaFree(flag_);
+  if (hsc_) cudaFreeHost(hsc_);
+}
+
+int CgEngine::ensure(const CgRun& run) {
+  const OpDev& op = *run.op;
+  if (op_ != run.op || nodes_ != op.nodes) {
+    cudaFree(r_);
+    cudaFree(p_);
+    cudaFree(w_);
+    r_ = p_ = w_ = nullptr;
+    CG_CUDA(cudaMalloc(&r_, sizeof(double) * op.nodes));
+    CG_CUDA(cudaMalloc(&p_, sizeof(double) * op.nodes));
+    CG_CUDA(cudaMalloc(&w_, sizeof(double) * op.nodes));
+    op_ = run.op;
+    nodes_ = op.nodes;
+    have_graph_ = false;
+  }
+  const int64_t need = 4 * std::max<int64_t>(std::max(k1_blocks(op), k2_blocks(op)), 2048);
+  if (partials_len_ < need) {
+    cudaFree(partials_);
+    CG_CUDA(cudaMalloc(&partials_, sizeof(double) * need));
+    partials_len_ = need;
+    have_graph_ = false;
+  }
+  if (!sc_) {
+    CG_CUDA(cudaMalloc(&sc_, sizeof(CgScalars)));
+    CG_CUDA(cudaMemset(sc_, 0, sizeof(CgScalars)));
+    CG_CUDA(cudaMallocHost(&hsc_, sizeof(CgScalars)));
+    CG_CUDA(cudaMalloc(&init_, 8 * sizeof(double)));
+    CG_CUDA(cudaMalloc(&flag_, sizeof(int)));
+  }
+  if (hist_len_ < (int64_t)run.max_it + 1) {
+    cudaFree(hist_);
+    hist_len_ = (int64_t)run.max_it + 1;
+    CG_CUDA(cudaMalloc(&hist_, sizeof(double) * hist_len_));
+    have_graph_ = false;
+  }
+  return SBX_OK;
+}
+
+int CgEngine::build_graph(const CgRun& run) {
+  const OpDev& op = *run.op;
+  if (exec_) cudaGraphExecDestroy(exec_);
+  if (graph_) cudaGraphDestroy(graph_);
+  exec_ = nullptr;
+  graph_ = nullptr;
+  CG_CUDA(cudaGraphCreate(&graph_, 0));
+  cudaGraphConditionalHandle handle;
+  CG_CUDA(cudaGraphConditionalHandleCreate(&handle, graph_, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams params = {};
+  params.type = cudaGraphNodeTypeConditional;
+  params.conditional.handle = handle;
+  params.conditional.type = cudaGraphCondTypeWhile;
+  params.conditional.size = 1;
+  cudaGraphNode_t node;
+  CG_CUDA(cudaGraphAddNode(&node, graph_, nullptr, 0, &params));
+  cudaGraph_t body = params.conditional.phGraph_out[0];
+  CG_CUDA(cudaStreamBeginCaptureToGraph(run.stream, body, nullptr, nullptr, 0,
+                                        cudaStreamCaptureModeRelaxed));
+  cudaError_t e1 = k1(op, r_, run.dinv, p_, run.x, w_, run.h1, run.h2, sc_, partials_,
+                      run.stream);
+  cudaError_t e2 = k2(op, w_, r_, run.dinv, sc_, partials_, hist_, hist_len_, handle, 1,
+                      run.stream);
+  cudaGraph_t captured = nullptr;
+  cudaError_t e3 = cudaStreamEndCapture(run.stream, &captured);
+  CG_CUDA(e1);
+  CG_CUDA(e2);
+  CG_CUDA(e3);
+  CG_CUDA(cudaGraphInstantiate(&exec_, graph_, 0));
+  key_ = Key{run.op, run.x, run.dinv, run.h1, run.h2, hist_, run.stream};
+  have_graph_ = true;
+  return SBX_OK;
+}
+
+int CgEngine::run_timed_loop(const CgRun& run) {
+  // Timing mode: the same two kernels launched from the host (no graph), each
+  // bracketed by CUDA events on the launching stream; one scalar read-back
+  // per iteration.  Used by bench.py for per-kernel durations.
+  const OpDev& op = *run.op;
+  cudaEvent_t ev[3];
+  for (auto& e : ev) CG_CUDA(cudaEventCreate(&e));
+  cudaGraphConditionalHandle none{};
+  for (;;) {
+    CG_CUDA(cudaEventRecord(ev[0], run.stream));
+    CG_CUDA(k1(op, r_, run.dinv, p_, run.x, w_, run.h1, run.h2, sc_, partials_, run.stream));
+    CG_CUDA(cudaEventRecord(ev[1], run.stream));
+    CG_CUDA(k2(op, w_, r_, run.dinv, sc_, partials_, hist_, hist_len_, none, 0, run.stream));
+    CG_CUDA(cudaEventRecord(ev[2], run.stream));
+    CG_CUDA(cudaMemcpyAsync(hsc_, sc_, sizeof(CgScalars), cudaMemcpyDeviceToHost, run.stream));
+    CG_CUDA(cudaEventSynchronize(ev[2]));
+    CG_CUDA(cudaStreamSynchronize(run.stream));
+    float a = 0, b = 0;
+    cudaEventElapsedTime(&a, ev[0], ev[1]);
+    cudaEventElapsedTime(&b, ev[1], ev[2]);
+    t_ax_ms_ += a;
+    t_upd_ms_ += b;
+    ++n_ax_;
+    ++n_upd_;
+    if (hsc_->done) break;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  return SBX_OK;
+}
+
+int CgEngine::solve(const CgRun& run, sbx_pcg_result* res) {
+  const OpDev& op = *run.op;
+  if (!run.interior_clean || op.n < 2 || op.n > 16) return kCgFallback;
+  if (ensure(run) != SBX_OK) return SBX_E_CUDA;
+  cudaStream_t s = run.stream;
+  const int64_t N = op.nodes;
+  // right-hand side must be continuous and masked for the fused p'Ap
+  CG_CUDA(cudaMemsetAsync(flag_, 0, sizeof(int), s));
+  if (op.nB > 0)
+    cg_check_rhs_kernel<<<(unsigned)((op.nB + 255) / 256), 256, 0, s>>>(op.b_off, op.b_idx,
+                                                                        op.nB, run.b, flag_);
+  // initial residual: r = b - A x0 (skipped for a zero guess: A 0 = 0)
+  // q = A x0 computed with the standalone operator into w_
+  CG_CUDA(launch_axhelm(op, run.x, w_, run.h1, run.h2, false, false, s));
+  CG_CUDA(launch_gs(op, w_, true, s));
+  const double* dinv = run.dinv;
+  {
+    int64_t blocks = std::min<int64_t>((N + 1023) / 1024, 1184);
+    if (blocks < 1) blocks = 1;
+    CG_CUDA(cudaMemsetAsync(&sc_->counter[2], 0, sizeof(uint32_t), s));
+    cg_init_kernel<<<(unsigned)blocks, 256, 0, s>>>(N, run.b, w_, dinv, op.inv_mult, r_,
+                                                    partials_, &sc_->counter[2], init_);
+    CG_CUDA(cudaGetLastError());
+  }
+  double hinit[4];
+  int hflag = 0;
+  CG_CUDA(cudaMemcpyAsync(hinit, init_, sizeof(hinit), cudaMemcpyDeviceToHost, s));
+  CG_CUDA(cudaMemcpyAsync(&hflag, flag_, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CG_CUDA(cudaStreamSynchronize(s));
+  if (hflag) return kCgFallback;
+  const double bb = hinit[0], bmb = hinit[1], rz = hinit[2], rr = hinit[3];
+  res->history_length = 0;
+  if (bb == 0.0) {
+    CG_CUDA(cudaMemsetAsync(run.x, 0, sizeof(double) * N, s));
+    CG_CUDA(cudaStreamSynchronize(s));
+    res->converged = 1;
+    return SBX_OK;
+  }
+  const double bnorm = std::sqrt(bb);
+  const double rnorm = std::sqrt(rr);
+  const double rel0 = rnorm / bnorm;
+  const double relp0 = bmb > 0.0 ? std::sqrt(std::max(rz, 0.0) / bmb) : 0.0;
+  CgScalars h{};
+  h.rz = rz;
+  h.rr = rr;
+  h.bnorm = bnorm;
+  h.bmb = bmb;
+  h.tol = run.tol;
+  h.rel = rel0;
+  h.relp = relp0;
+  h.it = 0;
+  h.max_it = run.max_it;
+  h.first = 1;
+  h.done = 0;
+  h.err_it = -1;
+  const bool conv0 = rel0 <= run.tol && relp0 <= run.tol;
+  if (conv0) {
+    h.converged = 1;
+    h.done = 1;
+  } else if (run.max_it <= 0) {
+    h.done = 1;
+  }
+  *hsc_ = h;
+  CG_CUDA(cudaMemcpyAsync(sc_, hsc_, sizeof(CgScalars), cudaMemcpyHostToDevice, s));
+  CG_CUDA(cudaMemcpyAsync(hist_, &rel0, sizeof(double), cudaMemcpyHostToDevice, s));
+  if (!h.done) {
+    if (run.timing) {
+      if (run_timed_loop(run) != SBX_OK) return SBX_E_CUDA;
+    } else {
+      const Key k{run.op, run.x, run.dinv, run.h1, run.h2, hist_, run.stream};
+      if (!have_graph_ || !(k == key_))
+        if (build_graph(run) != SBX_OK) return SBX_E_CUDA;
+      CG_CUDA(cudaGraphLaunch(exec_, s));
+    }
+    cg_finish_kernel<<<(unsigned)std::min<int64_t>((N + 255) / 256, 148 * 16), 256, 0, s>>>(
+        N, p_, run.x, sc_);
+    CG_CUDA(cudaGetLastError());
+  }
+  CG_CUDA(cudaMemcpyAsync(hsc_, sc_, sizeof(CgScalars), cudaMemcpyDeviceToHost, s));
+  CG_CUDA(cudaStreamSynchronize(s));
+  const CgScalars& o = *hsc_;
+  res->iterations = o.it;
+  res->converged = o.converged;
+  res->rel_residual = o.rel;
+  res->rel_residual_precond = o.relp;
+  res->history_length = (int64_t)o.it + 1;
+  if (run.history && run.history_capacity > 0) {
+    const int64_t cnt = std::min<int64_t>(res->history_length, run.history_capacity);
+    CG_CUDA(cudaMemcpy(run.history, hist_, sizeof(double) * cnt, cudaMemcpyDeviceToHost));
+  }
+  if (o.status == 5 || o.status == 6) {
+    res->error_iteration = o.err_it;
+    res->history_length = (int64_t)o.it + 1;
+    return o.status;
+  }
+  return SBX_OK;
+}
+
+int CgEngine::kernel_time(const char* name, double* total_ms, int64_t* launches) const {
+  const std::string nm = name ? name : "";
+  if (nm == "ax") {
+    *total_ms = t_ax_ms_;
+    *launches = n_ax_;
+  } else if (nm == "update") {
+    *total_ms = t_upd_ms_;
+    *launches = n_upd_;
+  } else {
+    return SBX_E_INVALID;
+  }
+  return SBX_OK;
+}
+
+}  // namespace sbx

@@ -1,0 +1,82 @@
+// Fused FAST PCG engine: two kernels per iteration, device-resident scalars,
+// the whole iteration loop in one CUDA graph with a conditional WHILE node.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/sbx.h"
+#include "kernels.cuh"
+
+namespace sbx {
+
+struct CgRun {
+  const OpDev* op = nullptr;
+  cudaStream_t stream = nullptr;
+  const double* b = nullptr;  // device
+  double* x = nullptr;        // device, initial guess in / solution out
+  const double* dinv = nullptr;  // 1/assembled diagonal, or null (no preconditioner)
+  double h1 = 1.0, h2 = 0.0, tol = 1e-8;
+  int max_it = 500;
+  double* history = nullptr;  // host
+  int64_t history_capacity = 0;
+  bool interior_clean = false;
+  bool timing = false;
+};
+
+// Returned by solve() when the FAST schedule's preconditions do not hold
+// (non-continuous / unmasked right-hand side, exotic maps): run EXACT instead.
+constexpr int kCgFallback = -1;
+
+class CgEngine {
+ public:
+  CgEngine() = default;
+  ~CgEngine();
+  int solve(const CgRun& run, sbx_pcg_result* res);
+  const std::string& error() const { return err_; }
+  int kernel_time(const char* name, double* total_ms, int64_t* launches) const;
+
+ private:
+  int ensure(const CgRun& run);
+  int build_graph(const CgRun& run);
+  int run_timed_loop(const CgRun& run);
+
+  const OpDev* op_ = nullptr;
+  int64_t nodes_ = 0;
+  double* r_ = nullptr;
+  double* p_ = nullptr;
+  double* w_ = nullptr;
+  double* partials_ = nullptr;
+  int64_t partials_len_ = 0;
+  CgScalars* sc_ = nullptr;
+  CgScalars* hsc_ = nullptr;  // pinned
+  double* hist_ = nullptr;    // device history
+  int64_t hist_len_ = 0;
+  double* init_ = nullptr;    // device init sums [4]
+  int* flag_ = nullptr;       // device continuity flag
+  // graph cache
+  cudaGraph_t graph_ = nullptr;
+  cudaGraphExec_t exec_ = nullptr;
+  struct Key {
+    const void* op;
+    const void* x;
+    const void* dinv;
+    double h1, h2;
+    const void* hist;
+    cudaStream_t stream;
+    bool operator==(const Key& o) const {
+      return op == o.op && x == o.x && dinv == o.dinv && h1 == o.h1 && h2 == o.h2 &&
+             hist == o.hist && stream == o.stream;
+    }
+  } key_{};
+  bool have_graph_ = false;
+  // per-kernel timing (timing mode)
+  double t_ax_ms_ = 0, t_upd_ms_ = 0;
+  int64_t n_ax_ = 0, n_upd_ = 0;
+  std::string err_;
+};
+
+}  // namespace sbx

@@ -1,0 +1,32 @@
+// Internal declarations shared by the host setup, the CUDA kernels and the
+// C ABI (include/sbx.h).  Not a public header.
+#pragma once
+
+#include <cstdint>
+#include <functional>
+#include <string>
+
+#include "../../include/sbx.h"
+
+namespace sbx {
+
+constexpr int kMaxDegree = 32;     // build_gll_basis limit (basis.cpp:11, 61-63)
+constexpr int kMaxTemplN = 15;     // tensor kernels are specialised for N <= 15 (n <= 16)
+
+void set_error(const std::string& msg);
+
+// host setup (setup.cpp)
+void host_parallel_for(int64_t n, const std::function<void(int64_t, int64_t)>& fn);
+int gll_basis(int degree, double* nodes, double* weights, double* deriv);
+int box_corners(int ex, int ey, int ez, const double* origin, const double* lengths,
+                double* corners);
+void deform_corners(int64_t elem_count, double a, double* corners);
+int geometric_factors(int64_t E, int degree, const double* corners, double* const g[6],
+                      double* bm, double* jac, int64_t* bad_elem);
+int gather_scatter(int ex, int ey, int ez, const int* periodic, int degree, int64_t* gid,
+                   int64_t* offsets, int64_t* group_nodes, int32_t* mult, double* inv_mult,
+                   int64_t* global_count);
+int dirichlet_mask(int ex, int ey, int ez, const int* periodic, int degree, double* mask);
+int partition_rcb(int64_t E, const double* corners, int ranks, int32_t* rank_of);
+
+}  // namespace sbx

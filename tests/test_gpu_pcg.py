@@ -1,0 +1,118 @@
+"""CUDA PCG against the reference: EXACT mode reproduces the whole residual
+history bit for bit; FAST mode converges in the same iteration count with the
+final residual and solution within 1e-10 relative (north_star)."""
+import hashlib
+
+import numpy as np
+import pytest
+
+import paper_2109_03592_b200 as sb
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+FINAL_TOL = 1e-10
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def case(golden, tag):
+    ex, ey, ez, N, h2, tol, deform, rnd = golden[f"{tag}_cfg"]
+    ex, ey, ez, N = int(ex), int(ey), int(ez), int(N)
+    ctx = sb.Context.box(ex, ey, ez, N, deform=deform)
+    P = O.Problem(ex, ey, ez, N, corners=O.box_corners(ex, ey, ez, deform=deform))
+    b = P.rhs_random_continuous(77) if rnd else P.rhs_manufactured(h2)
+    assert sha(b) == golden[f"{tag}_b_sha"][0]
+    return ctx, P, b, h2, tol
+
+
+TAGS = ["pcg_schwarz", "pcg_c1_manu", "pcg_c1_rand", "pcg_c1_rand12", "pcg_helm4",
+        "pcg_helm10"]
+
+
+@pytest.mark.parametrize("tag", TAGS)
+def test_pcg_exact_bitwise(cuda, golden, tag):
+    ctx, P, b, h2, tol = case(golden, tag)
+    op = sb.HelmholtzOperator(ctx, sb.HelmholtzCoeffs(1.0, h2))
+    x = np.zeros_like(b)
+    r = sb.pcg(op, b, x, sb.KrylovConfig(tol, 5000), mode="exact")
+    assert r.iterations == golden[f"{tag}_iterations"][0]
+    assert np.array_equal(np.array(r.residual_history), golden[f"{tag}_history"])
+    assert sha(x) == golden[f"{tag}_x_sha"][0]
+    assert r.converged
+
+
+@pytest.mark.parametrize("tag", TAGS)
+def test_pcg_fast_parity(cuda, golden, tag):
+    ctx, P, b, h2, tol = case(golden, tag)
+    op = sb.HelmholtzOperator(ctx, sb.HelmholtzCoeffs(1.0, h2))
+    x = np.zeros_like(b)
+    r = sb.pcg(op, b, x, sb.KrylovConfig(tol, 5000), mode="fast")
+    ref = P.pcg(b, 1.0, h2, "jacobi", tol, 5000)
+    assert r.converged
+    assert r.iterations == golden[f"{tag}_iterations"][0] == ref.iterations
+    assert r.rel_residual <= tol and r.rel_residual_precond <= tol
+    assert abs(r.rel_residual - ref.rel_residual) <= FINAL_TOL * max(tol, ref.rel_residual) * 1e3
+    hist = np.array(r.residual_history)
+    assert hist.shape == ref.residual_history.shape
+    np.testing.assert_allclose(hist, ref.residual_history, rtol=1e-6)
+    err = np.linalg.norm(x - ref.x) / np.linalg.norm(ref.x)
+    assert err <= FINAL_TOL
+
+
+def test_pcg_fast_device_tensors(cuda):
+    torch = cuda
+    ctx = sb.Context.box(4, 4, 4, 7, deform=0.05)
+    P = O.Problem(4, 4, 4, 7, corners=O.box_corners(4, 4, 4, deform=0.05))
+    b = P.rhs_random_continuous(3)
+    ref = P.pcg(b, tol=1e-9, max_iterations=2000)
+    xb = torch.zeros(P.nodes_count, dtype=torch.float64, device="cuda")
+    bd = torch.from_numpy(b).cuda()
+    op = sb.HelmholtzOperator(ctx)
+    r1 = sb.pcg(op, bd, xb, sb.KrylovConfig(1e-9, 2000))
+    assert r1.iterations == ref.iterations
+    # a second solve reuses the captured graph and must give identical bits
+    x2 = torch.zeros_like(xb)
+    r2 = sb.pcg(op, bd, x2, sb.KrylovConfig(1e-9, 2000))
+    assert r2.iterations == r1.iterations and torch.equal(x2, xb)
+
+
+def test_pcg_edge_cases(cuda):
+    ctx = sb.Context.box(2, 2, 2, 3)
+    P = O.Problem(2, 2, 2, 3)
+    op = sb.HelmholtzOperator(ctx)
+    for mode in ("exact", "fast"):
+        x = np.ones(P.nodes_count)
+        r = sb.pcg(op, np.zeros(P.nodes_count), x, sb.KrylovConfig(1e-8, 10), mode=mode)
+        assert r.converged and r.iterations == 0 and not x.any()  # krylov.cpp:11-16
+        b = P.rhs_random_continuous(5)
+        x = np.zeros_like(b)
+        r = sb.pcg(op, b, x, sb.KrylovConfig(1e-14, 1), mode=mode)
+        assert not r.converged and r.iterations == 1  # max_iterations reported, not raised
+        bn = b.copy()
+        bn[P.nper + 5] = np.nan
+        with pytest.raises(sb.SolverError) as ei:
+            sb.pcg(op, bn, np.zeros_like(b), sb.KrylovConfig(1e-8, 50), mode=mode)
+        assert ei.value.iteration == 0
+    # nonzero initial guess: r = b - A x0 (krylov.cpp:19-32)
+    b = P.rhs_random_continuous(6)
+    x0 = P.rhs_random_continuous(8)
+    ref = P.pcg(b, tol=1e-10, max_iterations=500, x0=x0)
+    for mode in ("exact", "fast"):
+        x = x0.copy()
+        r = sb.pcg(op, b, x, sb.KrylovConfig(1e-10, 500), mode=mode)
+        assert r.iterations == ref.iterations
+        if mode == "exact":
+            assert np.array_equal(x, ref.x)
+
+
+def test_pcg_fast_noncontinuous_rhs_falls_back(cuda):
+    ctx = sb.Context.box(2, 2, 2, 4)
+    P = O.Problem(2, 2, 2, 4)
+    b = O.fill_uniform(4, P.nodes_count)  # not continuous, not masked
+    ref = P.pcg(b, tol=1e-8, max_iterations=500)
+    x = np.zeros_like(b)
+    r = sb.pcg(sb.HelmholtzOperator(ctx), b, x, sb.KrylovConfig(1e-8, 500), mode="fast")
+    assert r.iterations == ref.iterations and np.array_equal(x, ref.x)
