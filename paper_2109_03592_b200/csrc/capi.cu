@@ -568,7 +568,20 @@ sbx_status sbx_ctx_create_box(const sbx_box_desc* d, int device, sbx_ctx** out) 
   pd.global_count = G;
   pd.group_offsets = offsets.data();
   pd.group_nodes = nodes.data();
-  return sbx_ctx_create(&pd, device, out);
+  SBX_TRY(sbx_ctx_create(&pd, device, out));
+  // structured element-centric gather-scatter (needs >= 2 cells per periodic axis)
+  const int counts[3] = {d->ex, d->ey, d->ez};
+  bool ok = true;
+  for (int q = 0; q < 3; ++q)
+    if (d->periodic[q] && counts[q] < 2) ok = false;
+  if (ok) {
+    (*out)->op.box = true;
+    (*out)->op.ex = d->ex;
+    (*out)->op.ey = d->ey;
+    (*out)->op.ez = d->ez;
+    for (int q = 0; q < 3; ++q) (*out)->op.per[q] = d->periodic[q] ? 1 : 0;
+  }
+  return SBX_OK;
 }
 
 void sbx_ctx_destroy(sbx_ctx* c) {

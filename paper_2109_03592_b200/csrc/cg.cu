@@ -19,10 +19,12 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
 #include "ax_core.cuh"
+#include "ax_tma.cuh"
 #include "cg.cuh"
 #include "sbx_internal.h"
 
@@ -70,6 +72,80 @@ __device__ double reduce_partials(const double* partials, int count, int stride,
   double s = 0.0;
   for (int q = threadIdx.x; q < count; q += blockDim.x) s += partials[(int64_t)q * stride + off];
   return cta_sum(s, sh);
+}
+
+// ------------------------------------------------ K1 (TMA pipeline) -----
+// Policy for ax_tma_kernel: stages r, p_old, x [, dinv] [, bm]; forms
+// z = r*dinv, p = z + beta*p_old (p = z on the first iteration), x +=
+// alpha_prev*p_old; epilogue writes w = A_local p and accumulates p.w.
+template <bool HAS_DINV, bool HAS_BM>
+struct CgK1Pol {
+  static constexpr int NV = 3 + (HAS_DINV ? 1 : 0) + (HAS_BM ? 1 : 0);
+  static constexpr int QD = 3;
+  static constexpr int QB = HAS_DINV ? 4 : 3;
+  struct Args {
+    const double* r;
+    const double* dinv;
+    double* p;
+    double* x;
+    double* w;
+    const double* bm;
+    double h2;
+    CgScalars* sc;
+    double beta, ap;
+    int first;
+  };
+  __device__ static bool init(Args& a) {
+    if (a.sc->done) return false;
+    a.first = a.sc->first;
+    a.beta = a.sc->beta;
+    a.ap = a.sc->alpha_prev;
+    return true;
+  }
+  __device__ static const double* vec(const Args& a, int q) {
+    return q == 0 ? a.r : q == 1 ? a.p : q == 2 ? a.x : (HAS_DINV && q == QD) ? a.dinv : a.bm;
+  }
+  __device__ static void pro(const Args& a, const double (&v)[NV], int64_t idx, double& u,
+                             double& hb) {
+    const double z = HAS_DINV ? v[0] * v[QD] : v[0];
+    if (a.first) {
+      u = z;
+    } else {
+      u = fma(a.beta, v[1], z);
+      a.x[idx] = fma(a.ap, v[1], v[2]);
+    }
+    a.p[idx] = u;
+    hb = HAS_BM ? a.h2 * v[QB] : 0.0;
+  }
+  __device__ static void epi(const Args& a, double acc, double u, double hb, int64_t idx,
+                             double& red) {
+    const double w = HAS_BM ? fma(hb, u, acc) : acc;
+    a.w[idx] = w;
+    red = fma(u, w, red);
+  }
+  __device__ static void finish(const Args& a, double red, double* partials, double* sh,
+                                bool* flag);
+};
+
+template <bool HAS_DINV, bool HAS_BM>
+__device__ void CgK1Pol<HAS_DINV, HAS_BM>::finish(const Args& a, double red, double* partials,
+                                                  double* sh, bool* flag) {
+  const double v = cta_sum(red, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = v;
+  CgScalars* sc = a.sc;
+  if (!last_block(&sc->counter[0], flag)) return;
+  const double tot = reduce_partials(partials, gridDim.x, 1, 0, sh);
+  if (threadIdx.x == 0) {
+    sc->counter[0] = 0;
+    sc->pq = tot;
+    if (!isfinite(tot) || tot <= 0.0) {
+      sc->status = 5;
+      sc->err_it = sc->it;
+      sc->done = 1;
+    } else {
+      sc->alpha = sc->rz / tot;
+    }
+  }
 }
 
 // ---------------------------------------------------------------- K1 -----
@@ -156,6 +232,160 @@ __device__ __forceinline__ void upd_node(double* __restrict__ r, const double* _
   rr = fma(rv * rv, wgt, rr);
 }
 
+// Shared tail of the update kernels: CTA partials of r'z and r'r, last-CTA
+// fixed-order reduction, beta, history, convergence / NaN tests
+// (krylov.cpp:51-57, 70-84) and the WHILE condition of the graph.
+__device__ __forceinline__ void update_tail(double rz, double rr, double alpha, double* red,
+                                            bool* is_last, CgScalars* __restrict__ sc,
+                                            double* __restrict__ partials,
+                                            double* __restrict__ hist, int64_t hist_cap,
+                                            cudaGraphConditionalHandle cond, int use_cond) {
+  rz = cta_sum(rz, red);
+  const double rz_b = rz;
+  rr = cta_sum(rr, red);
+  if (threadIdx.x == 0) {
+    partials[2 * (int64_t)blockIdx.x] = rz_b;
+    partials[2 * (int64_t)blockIdx.x + 1] = rr;
+  }
+  if (!last_block(&sc->counter[1], is_last)) return;
+  const double rz_new = reduce_partials(partials, gridDim.x, 2, 0, red);
+  const double rr_new = reduce_partials(partials, gridDim.x, 2, 1, red);
+  if (threadIdx.x == 0) {
+    sc->counter[1] = 0;
+    const double rnorm = sqrt(rr_new);
+    const int it = sc->it;
+    if (!isfinite(rnorm) || !isfinite(rz_new)) {
+      sc->status = 6;
+      sc->err_it = it;
+      sc->done = 1;
+    } else {
+      const double rel = rnorm / sc->bnorm;
+      if (hist && it + 1 < hist_cap) hist[it + 1] = rel;
+      sc->it = it + 1;
+      sc->beta = rz_new / sc->rz;
+      sc->rz = rz_new;
+      sc->rr = rr_new;
+      sc->alpha_prev = alpha;
+      sc->first = 0;
+      sc->rel = rel;
+      sc->relp = sc->bmb > 0.0 ? sqrt(fmax(rz_new, 0.0) / sc->bmb) : 0.0;
+      if (sc->rel <= sc->tol && sc->relp <= sc->tol) {
+        sc->converged = 1;
+        sc->done = 1;
+      } else if (sc->it >= sc->max_it) {
+        sc->done = 1;
+      }
+    }
+    if (use_cond) cudaGraphSetConditional(cond, sc->done ? 0 : 1);
+  }
+}
+
+struct BoxP {
+  int ex, ey, ez;
+  int px, py, pz;
+};
+
+// Per-direction sharing state of a node on the structured box: whether the
+// node is shared across this direction (act), the element-id delta to the
+// copy across the face (d), whether that copy comes first in the reference's
+// (element, local index) order (nfirst), and whether the node sits on a
+// non-periodic domain boundary (msk: Dirichlet).
+struct Dir {
+  int act;
+  bool nfirst;
+  bool msk;
+  int64_t d;
+};
+
+__device__ __forceinline__ Dir dir_state(int loc, int N, int c, int count, int per,
+                                         int64_t stride) {
+  Dir s{0, false, false, 0};
+  if (loc == 0) {
+    if (c > 0) {
+      s = Dir{1, true, false, -stride};
+    } else if (per) {
+      s = Dir{1, false, false, (int64_t)(count - 1) * stride};
+    } else {
+      s.msk = true;
+    }
+  } else if (loc == N) {
+    if (c < count - 1) {
+      s = Dir{1, false, false, stride};
+    } else if (per) {
+      s = Dir{1, true, false, -(int64_t)(count - 1) * stride};
+    } else {
+      s.msk = true;
+    }
+  }
+  return s;
+}
+
+// Structured-box update kernel: same work as cg_update_kernel but element-
+// centric (thread per (i,j) column, loop over k, coalesced r/w/dinv streams);
+// a shared node's assembled value is re-summed by every copy from the cell
+// lattice in the reference's copy order (z-side outer, y, x inner; smaller
+// element id first), so all copies get identical bits and no CSR is read.
+template <int n>
+__global__ void __launch_bounds__(AxCfg<n>::threads)
+    cg_update_box_kernel(const double* __restrict__ w, double* __restrict__ r,
+                         const double* __restrict__ dinv, int64_t E, BoxP bx,
+                         CgScalars* __restrict__ sc, double* __restrict__ partials,
+                         double* __restrict__ hist, int64_t hist_cap,
+                         cudaGraphConditionalHandle cond, int use_cond) {
+  using C = AxCfg<n>;
+  constexpr int N = n - 1;
+  __shared__ double red[32];
+  __shared__ bool is_last;
+  if (sc->done) {
+    if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0);
+    return;
+  }
+  const double alpha = sc->alpha;
+  const int t = threadIdx.x;
+  const int slot = t / C::nn, ij = t % C::nn, i = ij % n, j = ij / n;
+  const int64_t e = (int64_t)blockIdx.x * C::EPB + slot;
+  double rz = 0.0, rr = 0.0;
+  if (e < E && t < C::threads) {
+    const int ee = (int)e;
+    const int cx = ee % bx.ex, cy = (ee / bx.ex) % bx.ey, cz = ee / (bx.ex * bx.ey);
+    const int64_t exy = (int64_t)bx.ex * bx.ey;
+    const Dir X = dir_state(i, N, cx, bx.ex, bx.px, 1);
+    const Dir Y = dir_state(j, N, cy, bx.ey, bx.py, bx.ex);
+    const int64_t base = e * C::n3;
+#pragma unroll 1
+    for (int k = 0; k < n; ++k) {
+      const Dir Z = dir_state(k, N, cz, bx.ez, bx.pz, exy);
+      const int64_t a = base + k * C::nn + ij;
+      double q;
+      if (X.msk || Y.msk || Z.msk) {
+        q = 0.0;
+      } else if (!(X.act | Y.act | Z.act)) {
+        q = w[a];
+      } else {
+        double s = 0.0;
+        for (int zs = 0; zs <= Z.act; ++zs) {
+          const bool zn = Z.act && ((zs == 0) == Z.nfirst);
+          const int kk = zn ? N - k : k;
+          for (int ys = 0; ys <= Y.act; ++ys) {
+            const bool yn = Y.act && ((ys == 0) == Y.nfirst);
+            const int jj = yn ? N - j : j;
+            for (int xs = 0; xs <= X.act; ++xs) {
+              const bool xn = X.act && ((xs == 0) == X.nfirst);
+              const int ii = xn ? N - i : i;
+              const int64_t ce = e + (xn ? X.d : 0) + (yn ? Y.d : 0) + (zn ? Z.d : 0);
+              s += w[ce * C::n3 + (kk * n + jj) * n + ii];
+            }
+          }
+        }
+        q = s;
+      }
+      const double wgt = 1.0 / (double)(1 << (X.act + Y.act + Z.act));
+      upd_node(r, dinv, a, q, alpha, wgt, rz, rr);
+    }
+  }
+  update_tail(rz, rr, alpha, red, &is_last, sc, partials, hist, hist_cap, cond, use_cond);
+}
+
 template <int n>
 __global__ void __launch_bounds__(kUpdThreads)
     cg_update_kernel(const int32_t* __restrict__ b_off, const int32_t* __restrict__ b_idx,
@@ -210,44 +440,7 @@ __global__ void __launch_bounds__(kUpdThreads)
       }
     }
   }
-  rz = cta_sum(rz, red);
-  const double rz_b = rz;
-  rr = cta_sum(rr, red);
-  if (threadIdx.x == 0) {
-    partials[2 * (int64_t)blockIdx.x] = rz_b;
-    partials[2 * (int64_t)blockIdx.x + 1] = rr;
-  }
-  if (!last_block(&sc->counter[1], &is_last)) return;
-  const double rz_new = reduce_partials(partials, gridDim.x, 2, 0, red);
-  const double rr_new = reduce_partials(partials, gridDim.x, 2, 1, red);
-  if (threadIdx.x == 0) {
-    sc->counter[1] = 0;
-    const double rnorm = sqrt(rr_new);
-    const int it = sc->it;
-    if (!isfinite(rnorm) || !isfinite(rz_new)) {
-      sc->status = 6;
-      sc->err_it = it;
-      sc->done = 1;
-    } else {
-      const double rel = rnorm / sc->bnorm;
-      if (hist && it + 1 < hist_cap) hist[it + 1] = rel;
-      sc->it = it + 1;
-      sc->beta = rz_new / sc->rz;
-      sc->rz = rz_new;
-      sc->rr = rr_new;
-      sc->alpha_prev = alpha;
-      sc->first = 0;
-      sc->rel = rel;
-      sc->relp = sc->bmb > 0.0 ? sqrt(fmax(rz_new, 0.0) / sc->bmb) : 0.0;
-      if (sc->rel <= sc->tol && sc->relp <= sc->tol) {
-        sc->converged = 1;
-        sc->done = 1;
-      } else if (sc->it >= sc->max_it) {
-        sc->done = 1;
-      }
-    }
-    if (use_cond) cudaGraphSetConditional(cond, sc->done ? 0 : 1);
-  }
+  update_tail(rz, rr, alpha, red, &is_last, sc, partials, hist, hist_cap, cond, use_cond);
 }
 
 // x += alpha*p for the last completed iteration (K1 of the next iteration
@@ -312,14 +505,73 @@ __global__ void cg_check_rhs_kernel(const int32_t* __restrict__ b_off,
   }
 }
 
+// TMA pipeline eligibility: even n (16-byte aligned element blocks), 16-byte
+// aligned vectors, a layout that fits shared memory, and not disabled by
+// SBX_NO_TMA (used by the tests to cover both paths).
+inline bool aligned16(const void* p) { return p == nullptr || ((uintptr_t)p & 15) == 0; }
+
+bool k1_use_tma(const OpDev& op, const double* r, const double* dinv, const double* p,
+                const double* x, double h2) {
+  static const bool disabled = std::getenv("SBX_NO_TMA") != nullptr;
+  if (disabled || op.n % 2 != 0 || op.n > 16) return false;
+  return aligned16(r) && aligned16(dinv) && aligned16(p) && aligned16(x) && aligned16(op.G) &&
+         (h2 == 0.0 || aligned16(op.bm));
+}
+
+int g_num_sms[64] = {};
+
+int num_sms(int dev) {
+  if (!g_num_sms[dev & 63]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    g_num_sms[dev & 63] = v > 0 ? v : 148;
+  }
+  return g_num_sms[dev & 63];
+}
+
+template <int n, bool HAS_DINV, bool HAS_BM>
+cudaError_t launch_k1_tma(const OpDev& op, const double* r, const double* dinv, double* p,
+                          double* x, double* w, double h1, double h2, CgScalars* sc,
+                          double* partials, cudaStream_t s, int dev) {
+  using Pol = CgK1Pol<HAS_DINV, HAS_BM>;
+  using Ch = TmaChoice<n, Pol::NV>;
+  if constexpr (!Ch::ok) {
+    return cudaErrorNotSupported;
+  } else {
+    using L = TmaLayout<n, Pol::NV, Ch::GROUPS, Ch::S>;
+    auto kern = ax_tma_kernel<n, Pol, Ch::GROUPS, Ch::S>;
+    static bool attr_set[64] = {};
+    if (!attr_set[dev & 63]) {
+      cudaError_t err =
+          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::smem);
+      if (err != cudaSuccess) return err;
+      attr_set[dev & 63] = true;
+    }
+    DParam<n> Dp;
+    for (int q = 0; q < n * n; ++q) Dp.d[q] = op.Dh[q];
+    typename Pol::Args a{r, dinv, p, x, w, op.bm, h2, sc, 0.0, 0.0, 0};
+    const int64_t NG = (op.E + TmaGeom<n>::EPG - 1) / TmaGeom<n>::EPG;
+    int64_t grid = num_sms(dev);
+    if (grid > NG) grid = NG;
+    kern<<<(unsigned)grid, L::threads, L::smem, s>>>(a, op.G, op.E, h1, 1.0, Dp, partials);
+    return cudaGetLastError();
+  }
+}
+
 template <int n>
 cudaError_t launch_k1(const OpDev& op, const double* r, const double* dinv, double* p, double* x,
                       double* w, double h1, double h2, CgScalars* sc, double* partials,
                       cudaStream_t s) {
   using C = AxCfg<n>;
-  static bool attr_set[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
+  if (k1_use_tma(op, r, dinv, p, x, h2)) {
+    if (dinv && h2 != 0.0) return launch_k1_tma<n, true, true>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
+    if (dinv) return launch_k1_tma<n, true, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
+    if (h2 != 0.0) return launch_k1_tma<n, false, true>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
+    return launch_k1_tma<n, false, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
+  }
+  static bool attr_set[64] = {};
   if (!attr_set[dev & 63]) {
     cudaError_t err = cudaFuncSetAttribute(
         cg_ax_kernel<n>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem);
@@ -338,6 +590,14 @@ template <int n>
 cudaError_t launch_k2(const OpDev& op, const double* w, double* r, const double* dinv,
                       CgScalars* sc, double* partials, double* hist, int64_t hist_cap,
                       cudaGraphConditionalHandle cond, int use_cond, cudaStream_t s) {
+  if (op.box) {
+    using C = AxCfg<n>;
+    const int64_t blocks = (op.E + C::EPB - 1) / C::EPB;
+    BoxP bx{op.ex, op.ey, op.ez, op.per[0], op.per[1], op.per[2]};
+    cg_update_box_kernel<n><<<(unsigned)blocks, C::threads, 0, s>>>(
+        w, r, dinv, op.E, bx, sc, partials, hist, hist_cap, cond, use_cond);
+    return cudaGetLastError();
+  }
   const int64_t nBblocks = (op.nB + kUpdThreads - 1) / kUpdThreads;
   const int64_t m = n - 2;
   const int64_t nI = m > 0 ? op.E * m * m * m : 0;

@@ -26,6 +26,13 @@ struct OpDev {
   int64_t nBcopies = 0;
   const int32_t* b_off = nullptr;  // nB+1
   const int32_t* b_idx = nullptr;  // nBcopies
+  // Structured box (set when the map/mask are known to be build_gather_scatter /
+  // build_dirichlet_mask of an ex*ey*ez box): enables the element-centric
+  // gather-scatter that derives every copy from the cell lattice instead of
+  // reading the CSR.  Requires count_d >= 2 in every periodic direction.
+  bool box = false;
+  int ex = 0, ey = 0, ez = 0;
+  int per[3] = {0, 0, 0};
 };
 
 // Device-resident CG scalars for the fused (FAST) solver.

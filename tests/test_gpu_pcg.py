@@ -54,7 +54,8 @@ def test_pcg_fast_parity(cuda, golden, tag):
     assert r.converged
     assert r.iterations == golden[f"{tag}_iterations"][0] == ref.iterations
     assert r.rel_residual <= tol and r.rel_residual_precond <= tol
-    assert abs(r.rel_residual - ref.rel_residual) <= FINAL_TOL * max(tol, ref.rel_residual) * 1e3
+    # final relative residuals agree to 1e-10 (north_star); the solution to 1e-10 relative L2
+    assert abs(r.rel_residual - ref.rel_residual) <= FINAL_TOL
     hist = np.array(r.residual_history)
     assert hist.shape == ref.residual_history.shape
     np.testing.assert_allclose(hist, ref.residual_history, rtol=1e-6)
