@@ -47,6 +47,8 @@ struct sbx_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t own_stream = nullptr;
+  cudaStream_t caller = nullptr;  // stream the caller's inputs were produced on
+  cudaEvent_t order_ev = nullptr;
   OpDev op;
   int64_t global_count = 0;
   bool interior_clean = false;  // every element-interior node: unmasked singleton
@@ -133,6 +135,16 @@ sbx_status stage_in(sbx_ctx* c, const double* p, int slot, const double** out) {
   SBX_CUDA(cudaMemcpyAsync(w, p, sizeof(double) * (size_t)c->op.nodes, cudaMemcpyHostToDevice,
                            c->stream));
   *out = w;
+  return SBX_OK;
+}
+
+// Every entry point runs on the context's own (capturable, non-blocking)
+// stream, ordered after all work already queued on the caller's stream
+// (default: the legacy default stream, i.e. torch's default stream).
+sbx_status enter(sbx_ctx* c) {
+  SBX_CUDA(cudaSetDevice(c->device));
+  SBX_CUDA(cudaEventRecord(c->order_ev, c->caller));
+  SBX_CUDA(cudaStreamWaitEvent(c->stream, c->order_ev, 0));
   return SBX_OK;
 }
 
@@ -223,6 +235,7 @@ sbx_status ctx_init_common(sbx_ctx* c, int device) {
   SBX_CUDA(cudaSetDevice(device));
   SBX_CUDA(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
   c->stream = c->own_stream;
+  SBX_CUDA(cudaEventCreateWithFlags(&c->order_ev, cudaEventDisableTiming));
   void* p = nullptr;
   SBX_TRY(dalloc(c, &p, 64 * sizeof(double)));
   c->dscal = static_cast<double*>(p);
@@ -592,6 +605,7 @@ void sbx_ctx_destroy(sbx_ctx* c) {
   for (void* p : c->allocs) cudaFree(p);
   if (c->hscal) cudaFreeHost(c->hscal);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
+  if (c->order_ev) cudaEventDestroy(c->order_ev);
   delete c;
 }
 
@@ -608,7 +622,7 @@ sbx_status sbx_ctx_info(const sbx_ctx* c, int64_t* E, int32_t* n1d, int64_t* nod
 
 sbx_status sbx_ctx_set_stream(sbx_ctx* c, void* stream) {
   SBX_TRY(check_ctx(c));
-  c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
+  c->caller = static_cast<cudaStream_t>(stream);
   return SBX_OK;
 }
 
@@ -658,7 +672,7 @@ sbx_status sbx_axhelm(sbx_ctx* c, const double* u, double* w, double h1, double 
     set_error("axhelm: h2 != 0 needs the mass factors (bm)");
     return SBX_E_SHAPE;
   }
-  SBX_CUDA(cudaSetDevice(c->device));
+  SBX_TRY(enter(c));
   const double* du = nullptr;
   SBX_TRY(stage_in(c, u, 0, &du));
   const bool wdev = is_device_ptr(w);
@@ -678,7 +692,7 @@ sbx_status sbx_axhelm_diagonal(sbx_ctx* c, double h1, double h2, int assembled, 
     set_error("sbx_axhelm_diagonal: null output");
     return SBX_E_INVALID;
   }
-  SBX_CUDA(cudaSetDevice(c->device));
+  SBX_TRY(enter(c));
   const bool ddev = is_device_ptr(diag);
   double* dd = diag;
   if (!ddev) SBX_TRY(work(c, 1, &dd));
@@ -696,7 +710,7 @@ sbx_status sbx_gs_sum(sbx_ctx* c, double* f) {
     set_error("sbx_gs_sum: null field");
     return SBX_E_INVALID;
   }
-  SBX_CUDA(cudaSetDevice(c->device));
+  SBX_TRY(enter(c));
   const bool dev = is_device_ptr(f);
   double* df = f;
   if (!dev) {
@@ -722,7 +736,7 @@ sbx_status sbx_apply(sbx_ctx* c, const double* x, double* q, double h1, double h
     set_error("apply: h2 != 0 needs the mass factors (bm)");
     return SBX_E_SHAPE;
   }
-  SBX_CUDA(cudaSetDevice(c->device));
+  SBX_TRY(enter(c));
   const double* dx = nullptr;
   SBX_TRY(stage_in(c, x, 0, &dx));
   const bool qdev = is_device_ptr(q);
@@ -743,7 +757,7 @@ sbx_status sbx_dot(sbx_ctx* c, const double* a, const double* b, int weighted, u
     set_error("sbx_dot: null argument");
     return SBX_E_INVALID;
   }
-  SBX_CUDA(cudaSetDevice(c->device));
+  SBX_TRY(enter(c));
   const double *da = nullptr, *db = nullptr;
   SBX_TRY(stage_in(c, a, 0, &da));
   SBX_TRY(stage_in(c, b, 1, &db));
@@ -778,7 +792,7 @@ sbx_status sbx_pcg(sbx_ctx* c, const double* b, double* x, const sbx_pcg_config*
     set_error("pcg: h2 != 0 needs the mass factors (bm)");
     return SBX_E_SHAPE;
   }
-  SBX_CUDA(cudaSetDevice(c->device));
+  SBX_TRY(enter(c));
   std::memset(res, 0, sizeof(*res));
   res->error_iteration = -1;
   const int64_t N = c->op.nodes;

@@ -283,6 +283,7 @@ __device__ __forceinline__ void update_tail(double rz, double rr, double alpha, 
 struct BoxP {
   int ex, ey, ez;
   int px, py, pz;
+  int dbg;  // timing experiment only: skip the gathers (wrong result)
 };
 
 // Per-direction sharing state of a node on the structured box: whether the
@@ -320,6 +321,88 @@ __device__ __forceinline__ Dir dir_state(int loc, int N, int c, int count, int p
   return s;
 }
 
+// Flat structured-box update kernel: one node per thread, grid-stride, full
+// occupancy; a shared node's assembled value is re-summed by every copy from
+// the cell lattice in the reference's copy order (z-side outer, y, x inner;
+// smaller element id first), so every copy gets identical bits and no CSR is
+// read.  Own w/r/dinv streams are coalesced; partner copies are L2 hits.
+template <int n>
+__global__ void __launch_bounds__(kUpdThreads)
+    cg_update_flat_kernel(const double* __restrict__ w, double* __restrict__ r,
+                          const double* __restrict__ dinv, int64_t E, BoxP bx,
+                          CgScalars* __restrict__ sc, double* __restrict__ partials,
+                          double* __restrict__ hist, int64_t hist_cap,
+                          cudaGraphConditionalHandle cond, int use_cond) {
+  constexpr int N = n - 1;
+  constexpr int nn = n * n, n3 = n * n * n;
+  __shared__ double red[32];
+  __shared__ bool is_last;
+  if (sc->done) {
+    if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0);
+    return;
+  }
+  const double alpha = sc->alpha;
+  const int64_t exy = (int64_t)bx.ex * bx.ey;
+  const int64_t total = E * n3;
+  double rz = 0.0, rr = 0.0;
+  for (int64_t a = (int64_t)blockIdx.x * kUpdThreads + threadIdx.x; a < total;
+       a += (int64_t)gridDim.x * kUpdThreads) {
+    const uint32_t e = (uint32_t)(a / n3);
+    const int l = (int)(a - (int64_t)e * n3);
+    const int i = l % n, j = (l / n) % n, k = l / nn;
+    const double wo = __ldg(w + a);
+    const double ro = r[a];
+    const double dv = dinv ? __ldg(dinv + a) : 1.0;
+    const bool bnd = i == 0 || i == N || j == 0 || j == N || k == 0 || k == N;
+    double q = wo;
+    int cnt = 0;
+    if (bnd) {
+      const uint32_t cxy = e % (uint32_t)exy;
+      const int cx = (int)(cxy % (uint32_t)bx.ex), cy = (int)(cxy / (uint32_t)bx.ex);
+      const int cz = (int)(e / (uint32_t)exy);
+      const Dir X = dir_state(i, N, cx, bx.ex, bx.px, 1);
+      const Dir Y = dir_state(j, N, cy, bx.ey, bx.py, bx.ex);
+      const Dir Z = dir_state(k, N, cz, bx.ez, bx.pz, exy);
+      cnt = X.act + Y.act + Z.act;
+      if (X.msk || Y.msk || Z.msk) {
+        q = 0.0;
+      } else if (cnt) {
+        double s = 0.0;
+#pragma unroll
+        for (int zs = 0; zs < 2; ++zs) {
+          if (zs == 1 && !Z.act) break;
+          const bool zn = Z.act && ((zs == 0) == Z.nfirst);
+#pragma unroll
+          for (int ys = 0; ys < 2; ++ys) {
+            if (ys == 1 && !Y.act) break;
+            const bool yn = Y.act && ((ys == 0) == Y.nfirst);
+#pragma unroll
+            for (int xs = 0; xs < 2; ++xs) {
+              if (xs == 1 && !X.act) break;
+              const bool xn = X.act && ((xs == 0) == X.nfirst);
+              if (!zn && !yn && !xn) {
+                s += wo;
+              } else {
+                const int64_t ce = (int64_t)e + (xn ? X.d : 0) + (yn ? Y.d : 0) + (zn ? Z.d : 0);
+                const int kk = zn ? N - k : k, jj = yn ? N - j : j, ii = xn ? N - i : i;
+                s += __ldg(w + ce * n3 + (kk * n + jj) * n + ii);
+              }
+            }
+          }
+        }
+        q = s;
+      }
+    }
+    const double wgt = cnt == 0 ? 1.0 : cnt == 1 ? 0.5 : cnt == 2 ? 0.25 : 0.125;
+    const double rv = fma(-alpha, q, ro);
+    r[a] = rv;
+    const double z = rv * dv;
+    rz = fma(rv * z, wgt, rz);
+    rr = fma(rv * rv, wgt, rr);
+  }
+  update_tail(rz, rr, alpha, red, &is_last, sc, partials, hist, hist_cap, cond, use_cond);
+}
+
 // Structured-box update kernel: same work as cg_update_kernel but element-
 // centric (thread per (i,j) column, loop over k, coalesced r/w/dinv streams);
 // a shared node's assembled value is re-summed by every copy from the cell
@@ -343,44 +426,294 @@ __global__ void __launch_bounds__(AxCfg<n>::threads)
   const double alpha = sc->alpha;
   const int t = threadIdx.x;
   const int slot = t / C::nn, ij = t % C::nn, i = ij % n, j = ij / n;
-  const int64_t e = (int64_t)blockIdx.x * C::EPB + slot;
   double rz = 0.0, rr = 0.0;
+  // persistent grid-stride loop over element blocks: a few hundred CTAs, so
+  // the last-CTA ticket below is not a hot single-address atomic
+  const int64_t nEB = (E + C::EPB - 1) / C::EPB;
+  for (int64_t eb = blockIdx.x; eb < nEB; eb += gridDim.x) {
+  const int64_t e = eb * C::EPB + slot;
   if (e < E && t < C::threads) {
     const int ee = (int)e;
     const int cx = ee % bx.ex, cy = (ee / bx.ex) % bx.ey, cz = ee / (bx.ex * bx.ey);
     const int64_t exy = (int64_t)bx.ex * bx.ey;
-    const Dir X = dir_state(i, N, cx, bx.ex, bx.px, 1);
-    const Dir Y = dir_state(j, N, cy, bx.ey, bx.py, bx.ex);
-    const int64_t base = e * C::n3;
-#pragma unroll 1
+    const Dir none{0, false, false, 0};
+    const Dir X = bx.dbg ? none : dir_state(i, N, cx, bx.ex, bx.px, 1);
+    const Dir Y = bx.dbg ? none : dir_state(j, N, cy, bx.ey, bx.py, bx.ex);
+    const Dir Z0 = bx.dbg ? none : dir_state(0, N, cz, bx.ez, bx.pz, exy);
+    const Dir ZN = bx.dbg ? none : dir_state(N, N, cz, bx.ez, bx.pz, exy);
+    const bool mxy = X.msk || Y.msk;
+    // column pointers of the own copy and the copies across x, y and x+y
+    const double* pw = w + e * C::n3 + ij;
+    const double* px = w + (e + X.d) * C::n3 + j * n + (N - i);
+    const double* py = w + (e + Y.d) * C::n3 + (N - j) * n + i;
+    const double* pxy = w + (e + X.d + Y.d) * C::n3 + (N - j) * n + (N - i);
+    double* rp = r + e * C::n3 + ij;
+    const double* dp = dinv ? dinv + e * C::n3 + ij : nullptr;
+    const int cxy = X.act + Y.act;
+    // Load phase, branch-free (predicated): the element's own w, r, 1/diag
+    // columns and every partner copy this column needs (across x, y, x+y at
+    // all k; the four z-neighbour columns at the two z-faces).  Everything is
+    // in flight at once, so the gathers cost one latency, not one per k.
+    double wv[n], rvv[n], dv[n], wx[n], wy[n], wxy[n];
+    const bool axy = X.act && Y.act;
+#pragma unroll
     for (int k = 0; k < n; ++k) {
-      const Dir Z = dir_state(k, N, cz, bx.ez, bx.pz, exy);
-      const int64_t a = base + k * C::nn + ij;
+      wv[k] = __ldg(pw + k * C::nn);
+      rvv[k] = rp[k * C::nn];
+      dv[k] = dp ? __ldg(dp + k * C::nn) : 1.0;
+      wx[k] = X.act ? __ldg(px + k * C::nn) : 0.0;
+      wy[k] = Y.act ? __ldg(py + k * C::nn) : 0.0;
+      wxy[k] = axy ? __ldg(pxy + k * C::nn) : 0.0;
+    }
+    double z0[4], zN[4];
+    {
+      const double* cols[4] = {pw, px, py, pxy};
+      const bool on[4] = {true, X.act != 0, Y.act != 0, axy};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        z0[c] = (Z0.act && on[c]) ? __ldg(cols[c] + Z0.d * C::n3 + N * C::nn) : 0.0;
+        zN[c] = (ZN.act && on[c]) ? __ldg(cols[c] + ZN.d * C::n3) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < n; ++k) {
+      const bool zface = (k == 0 || k == N);
+      const Dir Z = k == 0 ? Z0 : (k == N ? ZN : Dir{0, false, false, 0});
       double q;
-      if (X.msk || Y.msk || Z.msk) {
+      if (mxy || (zface && Z.msk)) {
         q = 0.0;
-      } else if (!(X.act | Y.act | Z.act)) {
-        q = w[a];
+      } else if (cxy + Z.act == 0) {
+        q = wv[k];
       } else {
+        // copies in the reference order: z-side outer, y, x inner; within a
+        // direction the copy in the smaller cell first
         double s = 0.0;
-        for (int zs = 0; zs <= Z.act; ++zs) {
+#pragma unroll
+        for (int zs = 0; zs < 2; ++zs) {
+          if (zs == 1 && !Z.act) break;
           const bool zn = Z.act && ((zs == 0) == Z.nfirst);
-          const int kk = zn ? N - k : k;
-          for (int ys = 0; ys <= Y.act; ++ys) {
+#pragma unroll
+          for (int ys = 0; ys < 2; ++ys) {
+            if (ys == 1 && !Y.act) break;
             const bool yn = Y.act && ((ys == 0) == Y.nfirst);
-            const int jj = yn ? N - j : j;
-            for (int xs = 0; xs <= X.act; ++xs) {
+#pragma unroll
+            for (int xs = 0; xs < 2; ++xs) {
+              if (xs == 1 && !X.act) break;
               const bool xn = X.act && ((xs == 0) == X.nfirst);
-              const int ii = xn ? N - i : i;
-              const int64_t ce = e + (xn ? X.d : 0) + (yn ? Y.d : 0) + (zn ? Z.d : 0);
-              s += w[ce * C::n3 + (kk * n + jj) * n + ii];
+              const int c = (yn ? 2 : 0) + (xn ? 1 : 0);
+              const double v = zn ? (k == 0 ? z0[c] : zN[c])
+                                  : (c == 0 ? wv[k] : c == 1 ? wx[k] : c == 2 ? wy[k] : wxy[k]);
+              s += v;
             }
           }
         }
         q = s;
       }
-      const double wgt = 1.0 / (double)(1 << (X.act + Y.act + Z.act));
-      upd_node(r, dinv, a, q, alpha, wgt, rz, rr);
+      const int cnt = cxy + Z.act;
+      const double wgt = cnt == 0 ? 1.0 : cnt == 1 ? 0.5 : cnt == 2 ? 0.25 : 0.125;
+      const double rv = fma(-alpha, q, rvv[k]);
+      rp[k * C::nn] = rv;
+      const double z = rv * dv[k];
+      rz = fma(rv * z, wgt, rz);
+      rr = fma(rv * rv, wgt, rr);
+    }
+  }
+  }
+  update_tail(rz, rr, alpha, red, &is_last, sc, partials, hist, hist_cap, cond, use_cond);
+}
+
+// --------------------------------------------- K2 (TMA pipeline, box) -----
+// Same math as cg_update_box_kernel, but the element's own w, r, 1/diag
+// columns are streamed into shared memory by a producer warp with 1-D TMA
+// bulk copies (ring of slots owned per consumer group, as in ax_tma_kernel),
+// so HBM latency is hidden by the ring and registers stay free for the
+// partner-copy gathers, which hit L2.
+template <int n, int GROUPS, int SPG>
+struct K2Layout {
+  using T = TmaGeom<n>;
+  static constexpr int V_D = ((T::EPG * T::n3 + 1) / 2) * 2 + 2;
+  static constexpr int SLOT_D = 3 * V_D;
+  static constexpr int S = GROUPS * SPG;
+  static constexpr size_t BAR_BYTES = ((2 * S * 8 + 127) / 128) * 128;  // full[S] + empty[S]
+  static constexpr size_t smem = BAR_BYTES + sizeof(double) * (size_t)S * SLOT_D;
+  static constexpr int threads = GROUPS * T::TG + 32;
+};
+
+template <int n>
+struct K2Choice {
+  using T = TmaGeom<n>;
+  static constexpr size_t slot_bytes = sizeof(double) * K2Layout<n, 1, 1>::SLOT_D;
+  static constexpr int pick() {
+    for (int g = 16; g >= 1; --g) {
+      if (g * T::TG + 32 > 1024) continue;
+      if (g * T::TG > 384) continue;  // ~150 registers per consumer thread
+      if (256 + (size_t)g * 2 * slot_bytes <= 225 * 1024) return g;
+    }
+    return 1;
+  }
+  static constexpr int GROUPS = pick();
+  static constexpr int spg() {
+    const int p = (int)((225 * 1024 - 384) / (GROUPS * slot_bytes));
+    return p > 4 ? 4 : p;
+  }
+  static constexpr int SPG = spg();
+};
+
+template <int n, int GROUPS, int SPG>
+__global__ void __launch_bounds__(K2Layout<n, GROUPS, SPG>::threads, 1)
+    cg_update_tma_kernel(const double* __restrict__ w, double* __restrict__ r,
+                         const double* __restrict__ dinv, int64_t E, BoxP bx,
+                         CgScalars* __restrict__ sc, double* __restrict__ partials,
+                         double* __restrict__ hist, int64_t hist_cap,
+                         cudaGraphConditionalHandle cond, int use_cond) {
+  using T = TmaGeom<n>;
+  using L = K2Layout<n, GROUPS, SPG>;
+  constexpr int S = L::S;
+  constexpr int N = n - 1;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  __shared__ double red[32];
+  __shared__ bool is_last;
+  if (sc->done) {
+    if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0);
+    return;
+  }
+  const double alpha = sc->alpha;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
+  uint64_t* empty = full + S;
+  double* slots = reinterpret_cast<double*>(smraw + L::BAR_BYTES);
+  const int64_t NG = (E + T::EPG - 1) / T::EPG;
+  const int64_t M = NG > (int64_t)blockIdx.x ? (NG - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  double rz = 0.0, rr = 0.0;
+  const int warp = threadIdx.x >> 5;
+  if (warp == GROUPS * T::TG / 32) {
+    if ((threadIdx.x & 31) == 0) {
+      for (int64_t m = 0; m < M; ++m) {
+        const int s = (int)(m % S);
+        if (m >= S) mbar_wait(&empty[s], (uint32_t)((m / S - 1) & 1));
+        const int64_t e0 = (blockIdx.x + m * gridDim.x) * T::EPG;
+        const int64_t cnt = (E - e0) < T::EPG ? (E - e0) : T::EPG;
+        const int shift = (int)((e0 * T::n3) & 1);
+        const uint32_t vb = (uint32_t)((((cnt * T::n3 + shift) * 8) + 15) / 16 * 16);
+        double* slot = slots + s * L::SLOT_D;
+        mbar_expect_tx(&full[s], (dinv ? 3 : 2) * vb);
+        tma_load_1d(slot, w + e0 * T::n3 - shift, vb, &full[s]);
+        tma_load_1d(slot + L::V_D, r + e0 * T::n3 - shift, vb, &full[s]);
+        if (dinv) tma_load_1d(slot + 2 * L::V_D, dinv + e0 * T::n3 - shift, vb, &full[s]);
+      }
+    }
+  } else {
+    const int g = threadIdx.x / T::TG, lt = threadIdx.x % T::TG;
+    const int sl = lt / T::nn, ij = lt % T::nn, i = ij % n, j = ij / n;
+    const bool act = sl < T::EPG;
+    const int64_t exy = (int64_t)bx.ex * bx.ey;
+    for (int64_t m = g; m < M; m += GROUPS) {
+      const int s = (int)(m % S);
+      const int64_t e = (blockIdx.x + m * gridDim.x) * T::EPG + sl;
+      const bool valid = act && e < E;
+      // partner-copy addresses do not depend on the slot: issue the gathers
+      // before waiting for the TMA bytes
+      Dir X{0, false, false, 0}, Y = X, Z0 = X, ZN = X;
+      const double *pw = w, *px = w, *py = w, *pxy = w;
+      if (valid) {
+        const int ee = (int)e;
+        const int cx = ee % bx.ex, cy = (ee / bx.ex) % bx.ey, cz = ee / (bx.ex * bx.ey);
+        X = dir_state(i, N, cx, bx.ex, bx.px, 1);
+        Y = dir_state(j, N, cy, bx.ey, bx.py, bx.ex);
+        Z0 = dir_state(0, N, cz, bx.ez, bx.pz, exy);
+        ZN = dir_state(N, N, cz, bx.ez, bx.pz, exy);
+        pw = w + e * T::n3 + ij;
+        px = w + (e + X.d) * T::n3 + j * n + (N - i);
+        py = w + (e + Y.d) * T::n3 + (N - j) * n + i;
+        pxy = w + (e + X.d + Y.d) * T::n3 + (N - j) * n + (N - i);
+      }
+      const bool axy = X.act && Y.act;
+      double wx[n], wy[n], wxy[n];
+#pragma unroll
+      for (int k = 0; k < n; ++k) {
+        wx[k] = X.act ? __ldg(px + k * T::nn) : 0.0;
+        wy[k] = Y.act ? __ldg(py + k * T::nn) : 0.0;
+        wxy[k] = axy ? __ldg(pxy + k * T::nn) : 0.0;
+      }
+      double z0c0 = 0, z0c1 = 0, z0c2 = 0, z0c3 = 0, zNc0 = 0, zNc1 = 0, zNc2 = 0, zNc3 = 0;
+      if (Z0.act) {
+        const int64_t o = Z0.d * T::n3 + N * T::nn;
+        z0c0 = __ldg(pw + o);
+        if (X.act) z0c1 = __ldg(px + o);
+        if (Y.act) z0c2 = __ldg(py + o);
+        if (axy) z0c3 = __ldg(pxy + o);
+      }
+      if (ZN.act) {
+        const int64_t o = ZN.d * T::n3;
+        zNc0 = __ldg(pw + o);
+        if (X.act) zNc1 = __ldg(px + o);
+        if (Y.act) zNc2 = __ldg(py + o);
+        if (axy) zNc3 = __ldg(pxy + o);
+      }
+      mbar_wait(&full[s], (uint32_t)((m / S) & 1));
+      const int shift = (int)(((e - sl) * T::n3) & 1);
+      const double* slot = slots + s * L::SLOT_D + shift + sl * T::n3 + ij;
+      if (valid) {
+        const bool mxy = X.msk || Y.msk;
+        const int cxy = X.act + Y.act;
+        double* rp = r + e * T::n3 + ij;
+#pragma unroll
+        for (int k = 0; k < n; ++k) {
+          const double wo = slot[k * T::nn];
+          const double ro = slot[L::V_D + k * T::nn];
+          const double dv = dinv ? slot[2 * L::V_D + k * T::nn] : 1.0;
+          const Dir Z = k == 0 ? Z0 : (k == N ? ZN : Dir{0, false, false, 0});
+          double q;
+          if (mxy || ((k == 0 || k == N) && Z.msk)) {
+            q = 0.0;
+          } else if (cxy + Z.act == 0) {
+            q = wo;
+          } else {
+            double sum = 0.0;
+#pragma unroll
+            for (int zs = 0; zs < 2; ++zs) {
+              if (zs == 1 && !Z.act) break;
+              const bool zn = Z.act && ((zs == 0) == Z.nfirst);
+#pragma unroll
+              for (int ys = 0; ys < 2; ++ys) {
+                if (ys == 1 && !Y.act) break;
+                const bool yn = Y.act && ((ys == 0) == Y.nfirst);
+#pragma unroll
+                for (int xs = 0; xs < 2; ++xs) {
+                  if (xs == 1 && !X.act) break;
+                  const bool xn = X.act && ((xs == 0) == X.nfirst);
+                  double v;
+                  if (zn) {
+                    const bool lo = (k == 0);
+                    v = yn ? (xn ? (lo ? z0c3 : zNc3) : (lo ? z0c2 : zNc2))
+                           : (xn ? (lo ? z0c1 : zNc1) : (lo ? z0c0 : zNc0));
+                  } else {
+                    v = yn ? (xn ? wxy[k] : wy[k]) : (xn ? wx[k] : wo);
+                  }
+                  sum += v;
+                }
+              }
+            }
+            q = sum;
+          }
+          const int cnt = cxy + Z.act;
+          const double wgt = cnt == 0 ? 1.0 : cnt == 1 ? 0.5 : cnt == 2 ? 0.25 : 0.125;
+          const double rv = fma(-alpha, q, ro);
+          rp[k * T::nn] = rv;
+          const double z = rv * dv;
+          rz = fma(rv * z, wgt, rz);
+          rr = fma(rv * rv, wgt, rr);
+        }
+      }
+      named_bar_sync(1 + g, T::TG);
+      if (lt == 0) mbar_arrive(&empty[s]);
     }
   }
   update_tail(rz, rr, alpha, red, &is_last, sc, partials, hist, hist_cap, cond, use_cond);
@@ -590,10 +923,62 @@ template <int n>
 cudaError_t launch_k2(const OpDev& op, const double* w, double* r, const double* dinv,
                       CgScalars* sc, double* partials, double* hist, int64_t hist_cap,
                       cudaGraphConditionalHandle cond, int use_cond, cudaStream_t s) {
+  static const bool use_col = std::getenv("SBX_K2_COLUMN") != nullptr;
+  static const bool use_flat = std::getenv("SBX_K2_FLAT") != nullptr;
+  static const bool no_tma = std::getenv("SBX_NO_TMA") != nullptr;
+  if (op.box && !use_col && !use_flat && !no_tma && n % 2 == 0 && aligned16(w) &&
+      aligned16(r) && aligned16(dinv)) {
+    using Ch = K2Choice<n>;
+    using L = K2Layout<n, Ch::GROUPS, Ch::SPG>;
+    auto kern = cg_update_tma_kernel<n, Ch::GROUPS, Ch::SPG>;
+    static bool attr_set[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!attr_set[dev & 63]) {
+      cudaError_t err =
+          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::smem);
+      if (err != cudaSuccess) return err;
+      attr_set[dev & 63] = true;
+    }
+    const int64_t NG = (op.E + TmaGeom<n>::EPG - 1) / TmaGeom<n>::EPG;
+    int64_t grid = num_sms(dev);
+    if (grid > NG) grid = NG;
+    BoxP bx{op.ex, op.ey, op.ez, op.per[0], op.per[1], op.per[2], 0};
+    kern<<<(unsigned)grid, L::threads, L::smem, s>>>(w, r, dinv, op.E, bx, sc, partials, hist,
+                                                     hist_cap, cond, use_cond);
+    return cudaGetLastError();
+  }
+  if (op.box && use_flat) {
+    static int per_sm_f[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!per_sm_f[dev & 63]) {
+      int v = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, cg_update_flat_kernel<n>, kUpdThreads, 0);
+      per_sm_f[dev & 63] = v > 0 ? v : 1;
+    }
+    int64_t blocks = (op.nodes + kUpdThreads - 1) / kUpdThreads;
+    const int64_t cap = (int64_t)num_sms(dev) * per_sm_f[dev & 63];
+    if (blocks > cap) blocks = cap;
+    BoxP bx{op.ex, op.ey, op.ez, op.per[0], op.per[1], op.per[2], std::getenv("SBX_K2_NOGATHER") ? 1 : 0};
+    cg_update_flat_kernel<n><<<(unsigned)blocks, kUpdThreads, 0, s>>>(
+        w, r, dinv, op.E, bx, sc, partials, hist, hist_cap, cond, use_cond);
+    return cudaGetLastError();
+  }
   if (op.box) {
     using C = AxCfg<n>;
-    const int64_t blocks = (op.E + C::EPB - 1) / C::EPB;
-    BoxP bx{op.ex, op.ey, op.ez, op.per[0], op.per[1], op.per[2]};
+    static int per_sm[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!per_sm[dev & 63]) {
+      int v = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, cg_update_box_kernel<n>, C::threads, 0);
+      per_sm[dev & 63] = v > 0 ? v : 1;
+    }
+    int64_t blocks = (op.E + C::EPB - 1) / C::EPB;
+    const int64_t cap = (int64_t)num_sms(dev) * per_sm[dev & 63];
+    if (blocks > cap) blocks = cap;
+    BoxP bx{op.ex, op.ey, op.ez, op.per[0], op.per[1], op.per[2], std::getenv("SBX_K2_NOGATHER") ? 1 : 0};
     cg_update_box_kernel<n><<<(unsigned)blocks, C::threads, 0, s>>>(
         w, r, dinv, op.E, bx, sc, partials, hist, hist_cap, cond, use_cond);
     return cudaGetLastError();
