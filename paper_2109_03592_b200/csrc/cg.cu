@@ -823,6 +823,14 @@ __global__ void cg_init_kernel(int64_t N, const double* __restrict__ b,
 // Continuity + mask check of the right-hand side on the boundary groups: the
 // fused p'Ap identity needs b (hence r, z, p) equal on all copies and zero
 // on masked copies.  flag := 1 on violation.
+__global__ void cg_any_nonzero_kernel(int64_t N, const double* __restrict__ x, int* flag) {
+  bool nz = false;
+  for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < N;
+       a += (int64_t)gridDim.x * blockDim.x)
+    nz |= (x[a] != 0.0);
+  if (__syncthreads_or(nz) && threadIdx.x == 0) *flag = 1;
+}
+
 __global__ void cg_check_rhs_kernel(const int32_t* __restrict__ b_off,
                                     const int32_t* __restrict__ b_idx, int64_t nB,
                                     const double* __restrict__ b, int* flag) {
@@ -1098,7 +1106,7 @@ int CgEngine::ensure(const CgRun& run) {
     CG_CUDA(cudaMemset(sc_, 0, sizeof(CgScalars)));
     CG_CUDA(cudaMallocHost(&hsc_, sizeof(CgScalars)));
     CG_CUDA(cudaMalloc(&init_, 8 * sizeof(double)));
-    CG_CUDA(cudaMalloc(&flag_, sizeof(int)));
+    CG_CUDA(cudaMalloc(&flag_, 4 * sizeof(int)));
   }
   if (hist_len_ < (int64_t)run.max_it + 1) {
     cudaFree(hist_);
@@ -1184,16 +1192,25 @@ int CgEngine::solve(const CgRun& run, sbx_pcg_result* res) {
   if (op.nB > 0)
     cg_check_rhs_kernel<<<(unsigned)((op.nB + 255) / 256), 256, 0, s>>>(op.b_off, op.b_idx,
                                                                         op.nB, run.b, flag_);
-  // initial residual: r = b - A x0 (skipped for a zero guess: A 0 = 0)
-  // q = A x0 computed with the standalone operator into w_
-  CG_CUDA(launch_axhelm(op, run.x, w_, run.h1, run.h2, false, false, s));
-  CG_CUDA(launch_gs(op, w_, true, s));
+  // initial residual: r = b - A x0, the apply skipped for a zero guess
+  // (krylov.cpp:19-32: any entry != 0, NaN included, counts as nonzero)
+  CG_CUDA(cudaMemsetAsync(flag_ + 1, 0, sizeof(int), s));
+  cg_any_nonzero_kernel<<<(unsigned)std::min<int64_t>((N + 255) / 256, 148 * 8), 256, 0, s>>>(
+      N, run.x, flag_ + 1);
+  int hnz = 0;
+  CG_CUDA(cudaMemcpyAsync(&hnz, flag_ + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CG_CUDA(cudaStreamSynchronize(s));
+  if (hnz) {
+    CG_CUDA(launch_axhelm(op, run.x, w_, run.h1, run.h2, false, false, s));
+    CG_CUDA(launch_gs(op, w_, true, s));
+  }
   const double* dinv = run.dinv;
   {
     int64_t blocks = std::min<int64_t>((N + 1023) / 1024, 1184);
     if (blocks < 1) blocks = 1;
     CG_CUDA(cudaMemsetAsync(&sc_->counter[2], 0, sizeof(uint32_t), s));
-    cg_init_kernel<<<(unsigned)blocks, 256, 0, s>>>(N, run.b, w_, dinv, op.inv_mult, r_,
+    cg_init_kernel<<<(unsigned)blocks, 256, 0, s>>>(N, run.b, hnz ? w_ : nullptr, dinv,
+                                                    op.inv_mult, r_,
                                                     partials_, &sc_->counter[2], init_);
     CG_CUDA(cudaGetLastError());
   }
