@@ -203,19 +203,38 @@ sbx_status sbx_pcg(sbx_ctx* ctx, const double* b, double* x, const sbx_pcg_confi
                    sbx_pcg_result* result);
 
 /* -------------------------------------------------------- multi-GPU ------ */
-/* One process per GPU.  The application (or torch.distributed, see
- * paper_2109_03592_b200/dist.py) distributes the 128-byte NCCL id from rank 0. */
-sbx_status sbx_comm_unique_id(uint8_t id[128]);
+/* One process per GPU; elements of a structured box are partitioned by
+ * partition_rcb (mesh.cpp:168-226).  Shared nodes on rank boundaries are
+ * assembled from raw copy values exchanged over peer memory (CUDA IPC windows
+ * written directly by the kernels over NVLink), summed on every rank in the
+ * reference's canonical copy order (bitwise the single-process gs_sum).  CG
+ * scalars are exchanged the same way and summed in rank order.
+ *
+ * Exchange plan (host only, no GPU needed; used by the tests): */
+typedef struct sbx_dist_plan sbx_dist_plan;
+sbx_status sbx_dist_plan_create(const sbx_box_desc* desc, const int32_t* rank_of, int nranks,
+                                int rank, sbx_dist_plan** out);
+void sbx_dist_plan_destroy(sbx_dist_plan* plan);
+/* [local elements, local nodes, boundary groups, boundary copies, interface
+ *  groups, interface copies, neighbours, receive total, send total] */
+sbx_status sbx_dist_plan_sizes(const sbx_dist_plan* plan, int64_t sizes[9]);
+/* 0 loc_elems (i64) | 1 b_off 2 b_idx 3 if_off 4 if_code 5 nbr (i32) | 6 send
+ * counts (i64) | 7 send_idx (i32) | 8 recv_count 9 recv_base (i64) | 10 nbr27
+ * (i32) | 11 inv_mult 12 mask (f64) | 13 if_gid (i64) */
+sbx_status sbx_dist_plan_array(const sbx_dist_plan* plan, int which, void* out);
 
-/* Distributed context: this rank's elements of a structured box partitioned
- * by partition_rcb (rank_of[E_global] as produced by sbx_partition_rcb).
- * Builds the local map and the cross-rank gather-scatter exchange plan;
- * requires an NCCL communicator (id from sbx_comm_unique_id on rank 0). */
+/* Distributed context: this rank's part of the box, device data + a peer
+ * window.  Connect it with the windows of all ranks (blobs gathered by the
+ * application, e.g. torch.distributed.all_gather_object) before any call. */
 sbx_status sbx_ctx_create_box_dist(const sbx_box_desc* desc, const int32_t* rank_of,
-                                   int nranks, int rank, const uint8_t id[128], int device,
-                                   sbx_ctx** out);
+                                   int nranks, int rank, int device, sbx_ctx** out);
+/* size of one rank's window blob; this rank's blob */
+size_t sbx_ctx_dist_blob_size(int nranks);
+sbx_status sbx_ctx_dist_blob(sbx_ctx* ctx, uint8_t* blob);
+/* blobs: nranks * sbx_ctx_dist_blob_size(nranks) bytes, rank order */
+sbx_status sbx_ctx_dist_connect(sbx_ctx* ctx, const uint8_t* blobs);
 
-/* local element ids (global numbering, ascending) of a distributed context */
+/* local element ids (global numbering, ascending) of a context */
 sbx_status sbx_ctx_local_elements(const sbx_ctx* ctx, int64_t* global_ids);
 
 /* --------------------------------------------------------- instrumentation */

@@ -79,8 +79,14 @@ _sig("sbx_apply", _i, _vp, _vp, _vp, _d, _d, _u32)
 _sig("sbx_dot", _i, _vp, _vp, _vp, _i, _u32, C.POINTER(_d))
 _sig("sbx_pcg_config_default", None, C.POINTER(PcgConfig))
 _sig("sbx_pcg", _i, _vp, _vp, _vp, C.POINTER(PcgConfig), C.POINTER(PcgResultC))
-_sig("sbx_comm_unique_id", _i, _vp)
-_sig("sbx_ctx_create_box_dist", _i, C.POINTER(BoxDesc), _vp, _i, _i, _vp, _i, C.POINTER(_vp))
+_sig("sbx_dist_plan_create", _i, C.POINTER(BoxDesc), _vp, _i, _i, C.POINTER(_vp))
+_sig("sbx_dist_plan_destroy", None, _vp)
+_sig("sbx_dist_plan_sizes", _i, _vp, _vp)
+_sig("sbx_dist_plan_array", _i, _vp, _i, _vp)
+_sig("sbx_ctx_create_box_dist", _i, C.POINTER(BoxDesc), _vp, _i, _i, _i, C.POINTER(_vp))
+_sig("sbx_ctx_dist_blob_size", C.c_size_t, _i)
+_sig("sbx_ctx_dist_blob", _i, _vp, _vp)
+_sig("sbx_ctx_dist_connect", _i, _vp, _vp)
 _sig("sbx_ctx_local_elements", _i, _vp, _vp)
 _sig("sbx_ctx_enable_timing", _i, _vp, _i)
 _sig("sbx_ctx_kernel_time", _i, _vp, C.c_char_p, C.POINTER(_d), C.POINTER(_i64))

@@ -71,6 +71,13 @@ struct sbx_ctx {
   std::unique_ptr<CgEngine> cg;
   // distributed (filled by sbx_ctx_create_box_dist)
   std::vector<int64_t> local_elements;
+  bool dist = false;
+  bool connected = false;
+  int nranks = 1, rank = 0;
+  DistDev dd;
+  void* window = nullptr;
+  std::vector<int64_t> recv_base_for_src;  // per source rank, -1 if not a neighbour
+  std::vector<void*> peer_windows;
   // timing
   bool timing = false;
 };
@@ -319,11 +326,25 @@ sbx_status dot_exact(sbx_ctx* c, const double* a, const double* b, bool weighted
   return SBX_OK;
 }
 
+// gather-scatter of a device field: local boundary CSR, plus the peer
+// exchange and interface groups on a distributed context
+sbx_status gs_dev(sbx_ctx* c, double* f, bool apply_mask) {
+  if (c->dist) {
+    if (!c->connected) {
+      set_error("distributed context used before sbx_ctx_dist_connect");
+      return SBX_E_COMM;
+    }
+    SBX_CUDA(launch_dist_gs(c->op, c->dd, f, apply_mask && c->has_mask, c->stream));
+  } else {
+    SBX_CUDA(launch_gs(c->op, f, apply_mask && c->has_mask, c->stream));
+  }
+  return SBX_OK;
+}
+
 sbx_status apply_dev(sbx_ctx* c, const double* x, double* q, double h1, double h2,
                      bool exact, bool flip, bool use_mask) {
   SBX_CUDA(launch_axhelm(c->op, x, q, h1, h2, exact, flip, c->stream));
-  SBX_CUDA(launch_gs(c->op, q, use_mask && c->has_mask, c->stream));
-  return SBX_OK;
+  return gs_dev(c, q, use_mask);
 }
 
 sbx_status ensure_diag(sbx_ctx* c, double h1, double h2) {
@@ -336,7 +357,7 @@ sbx_status ensure_diag(sbx_ctx* c, double h1, double h2) {
     c->ddinv = static_cast<double*>(p);
   }
   SBX_CUDA(launch_axhelm_diag(c->op, h1, h2, c->ddiag, c->stream));
-  SBX_CUDA(launch_gs(c->op, c->ddiag, false, c->stream));
+  SBX_TRY(gs_dev(c, c->ddiag, false));
   SBX_CUDA(launch_recip(c->op.nodes, c->ddiag, c->ddinv, c->stream));
   c->diag_h1 = h1;
   c->diag_h2 = h2;
@@ -602,6 +623,8 @@ void sbx_ctx_destroy(sbx_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   c->cg.reset();
+  for (void* p : c->peer_windows) cudaIpcCloseMemHandle(p);
+  if (c->window) cudaFree(c->window);
   for (void* p : c->allocs) cudaFree(p);
   if (c->hscal) cudaFreeHost(c->hscal);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
@@ -697,7 +720,7 @@ sbx_status sbx_axhelm_diagonal(sbx_ctx* c, double h1, double h2, int assembled, 
   double* dd = diag;
   if (!ddev) SBX_TRY(work(c, 1, &dd));
   SBX_CUDA(launch_axhelm_diag(c->op, h1, h2, dd, c->stream));
-  if (assembled) SBX_CUDA(launch_gs(c->op, dd, false, c->stream));
+  if (assembled) SBX_TRY(gs_dev(c, dd, false));
   if (!ddev)
     SBX_CUDA(cudaMemcpyAsync(diag, dd, sizeof(double) * (size_t)c->op.nodes,
                              cudaMemcpyDeviceToHost, c->stream));
@@ -718,7 +741,7 @@ sbx_status sbx_gs_sum(sbx_ctx* c, double* f) {
     SBX_CUDA(cudaMemcpyAsync(df, f, sizeof(double) * (size_t)c->op.nodes,
                              cudaMemcpyHostToDevice, c->stream));
   }
-  SBX_CUDA(launch_gs(c->op, df, false, c->stream));
+  SBX_TRY(gs_dev(c, df, false));
   if (!dev)
     SBX_CUDA(cudaMemcpyAsync(f, df, sizeof(double) * (size_t)c->op.nodes, cudaMemcpyDeviceToHost,
                              c->stream));
@@ -761,9 +784,16 @@ sbx_status sbx_dot(sbx_ctx* c, const double* a, const double* b, int weighted, u
   const double *da = nullptr, *db = nullptr;
   SBX_TRY(stage_in(c, a, 0, &da));
   SBX_TRY(stage_in(c, b, 1, &db));
-  if (flags & SBX_FLAG_EXACT) return dot_exact(c, da, db, weighted != 0, result);
+  if (flags & SBX_FLAG_EXACT) {
+    if (c->dist) {
+      set_error("sbx_dot: the reference-order (EXACT) dot is single-process");
+      return SBX_E_CONFIG;
+    }
+    return dot_exact(c, da, db, weighted != 0, result);
+  }
   SBX_CUDA(launch_dot_fast(c->op.nodes, da, db, weighted ? c->op.inv_mult : nullptr,
                            c->partials, c->dcount, c->dscal, c->stream));
+  if (c->dist) SBX_CUDA(launch_dist_allreduce(c->dd, 3, c->dscal, c->dscal, 1, c->stream));
   SBX_CUDA(cudaMemcpyAsync(c->hscal, c->dscal, sizeof(double), cudaMemcpyDeviceToHost,
                            c->stream));
   SBX_TRY(finish(c));
@@ -806,6 +836,14 @@ sbx_status sbx_pcg(sbx_ctx* c, const double* b, double* x, const sbx_pcg_config*
                              c->stream));
   }
   sbx_status st;
+  if (c->dist && cfg->mode != SBX_MODE_FAST) {
+    set_error("pcg: the EXACT (reference-order) mode is single-process; use FAST with >1 rank");
+    return SBX_E_CONFIG;
+  }
+  if (c->dist && !c->connected) {
+    set_error("distributed context used before sbx_ctx_dist_connect");
+    return SBX_E_COMM;
+  }
   if (cfg->mode == SBX_MODE_FAST) {
     if (cfg->precond == SBX_PRECOND_JACOBI) SBX_TRY(ensure_diag(c, cfg->h1, cfg->h2));
     CgRun run;
@@ -822,6 +860,7 @@ sbx_status sbx_pcg(sbx_ctx* c, const double* b, double* x, const sbx_pcg_config*
     run.history_capacity = cfg->history_capacity;
     run.interior_clean = c->interior_clean;
     run.timing = c->timing;
+    run.dist = c->dist ? &c->dd : nullptr;
     const int rc = c->cg->solve(run, res);
     st = (sbx_status)rc;
     if (rc == kCgFallback) {
@@ -836,7 +875,7 @@ sbx_status sbx_pcg(sbx_ctx* c, const double* b, double* x, const sbx_pcg_config*
     else if (st == SBX_E_NAN)
       set_error("pcg: residual diverged (NaN/Inf) at iteration " +
                 std::to_string(res->error_iteration));
-    else if (st == SBX_E_SHAPE) set_error(c->cg->error());
+    else if (st == SBX_E_SHAPE || st == SBX_E_COMM) set_error(c->cg->error());
   } else {
     st = pcg_exact(c, db, dx, cfg, res);
   }
@@ -875,3 +914,241 @@ sbx_status sbx_ctx_local_elements(const sbx_ctx* c, int64_t* ids) {
 }  // extern "C"
 
 // ---- multi-GPU entry points: see dist.cu -----------------------------------
+
+// =========================================================== multi-GPU =====
+#include "dist_plan.h"
+
+namespace {
+
+struct DistBlob {
+  cudaIpcMemHandle_t handle;
+  int64_t recv_total;
+  int64_t recv_base_for_src[kMaxRanks];
+};
+
+sbx_status upload_dist(sbx_ctx* c, const DistPlan& P, const sbx_box_desc* d) {
+  const int n = P.n;
+  const int64_t EL = (int64_t)P.loc_elems.size();
+  const int64_t NL = P.nodes_local();
+  c->op.E = EL;
+  c->op.n = n;
+  c->op.nodes = NL;
+  c->global_count = 0;
+  // local geometry from the local elements' corners (deformed like the box)
+  std::vector<double> all(P.E * 24);
+  SBX_TRY(sbx_box_corners(d->ex, d->ey, d->ez, d->origin, d->lengths, all.data()));
+  if (d->deform_amplitude != 0.0) deform_corners(P.E, d->deform_amplitude, all.data());
+  std::vector<double> loc(EL * 24);
+  for (int64_t le = 0; le < EL; ++le)
+    std::memcpy(&loc[le * 24], &all[P.loc_elems[le] * 24], 24 * sizeof(double));
+  all.clear();
+  all.shrink_to_fit();
+  std::vector<double> deriv(n * n);
+  SBX_TRY(sbx_gll_basis(d->degree, nullptr, nullptr, deriv.data()));
+  for (int q = 0; q < n * n; ++q) c->op.Dh[q] = deriv[q];
+  double* dD = nullptr;
+  SBX_TRY(dupload(c, &dD, deriv.data(), (int64_t)n * n));
+  c->op.Dd = dD;
+  std::vector<std::vector<double>> g(7, std::vector<double>(NL));
+  int64_t bad = -1;
+  SBX_TRY(sbx_geometric_factors(EL, d->degree, loc.data(), g[0].data(), g[1].data(),
+                                g[2].data(), g[3].data(), g[4].data(), g[5].data(), g[6].data(),
+                                nullptr, &bad));
+  double* G = nullptr;
+  SBX_TRY(dupload<double>(c, &G, nullptr, 6 * NL));
+  {
+    double* tmp[6] = {};
+    for (int q = 0; q < 6; ++q) {
+      SBX_CUDA(cudaMalloc(&tmp[q], sizeof(double) * (size_t)NL));
+      SBX_CUDA(cudaMemcpyAsync(tmp[q], g[q].data(), sizeof(double) * (size_t)NL,
+                               cudaMemcpyHostToDevice, c->stream));
+    }
+    SBX_CUDA(launch_pack_geometry(c->op, tmp, G, c->stream));
+    SBX_CUDA(cudaStreamSynchronize(c->stream));
+    for (int q = 0; q < 6; ++q) cudaFree(tmp[q]);
+  }
+  c->op.G = G;
+  double *bm = nullptr, *mask = nullptr, *im = nullptr;
+  SBX_TRY(dupload(c, &bm, g[6].data(), NL));
+  SBX_TRY(dupload(c, &mask, P.mask.data(), NL));
+  SBX_TRY(dupload(c, &im, P.inv_mult.data(), NL));
+  c->op.bm = bm;
+  c->op.mask = mask;
+  c->op.inv_mult = im;
+  c->has_mask = true;
+  c->interior_clean = true;  // by construction of the plan
+  int32_t *boff = nullptr, *bidx = nullptr, *n27 = nullptr;
+  SBX_TRY(dupload(c, &boff, P.b_off.data(), (int64_t)P.b_off.size()));
+  SBX_TRY(dupload(c, &bidx, P.b_idx.data(), (int64_t)P.b_idx.size()));
+  SBX_TRY(dupload(c, &n27, P.nbr27.data(), (int64_t)P.nbr27.size()));
+  int64_t* ge = nullptr;
+  SBX_TRY(dupload(c, &ge, P.loc_elems.data(), EL));
+  c->op.b_off = boff;
+  c->op.b_idx = bidx;
+  c->op.nB = (int64_t)P.b_off.size() - 1;
+  c->op.nBcopies = (int64_t)P.b_idx.size();
+  c->op.box = true;
+  c->op.table = true;
+  c->op.ex = d->ex;
+  c->op.ey = d->ey;
+  c->op.ez = d->ez;
+  for (int q = 0; q < 3; ++q) c->op.per[q] = d->periodic[q] ? 1 : 0;
+  c->op.nbr27 = n27;
+  c->op.gelem = ge;
+  // exchange plan on the device
+  DistDev& D = c->dd;
+  D.nranks = P.nranks;
+  D.rank = P.rank;
+  D.nodes_local = NL;
+  D.nnbr = (int)P.nbr.size();
+  std::vector<int32_t> sidx;
+  D.send_off[0] = 0;
+  for (int qi = 0; qi < D.nnbr; ++qi) {
+    D.nbr[qi] = P.nbr[qi];
+    sidx.insert(sidx.end(), P.send_idx[qi].begin(), P.send_idx[qi].end());
+    D.send_off[qi + 1] = (int64_t)sidx.size();
+  }
+  int32_t *dsidx = nullptr, *ioff = nullptr, *icode = nullptr;
+  SBX_TRY(dupload(c, &dsidx, sidx.data(), (int64_t)sidx.size()));
+  SBX_TRY(dupload(c, &ioff, P.if_off.data(), (int64_t)P.if_off.size()));
+  SBX_TRY(dupload(c, &icode, P.if_code.data(), (int64_t)P.if_code.size()));
+  D.send_idx = dsidx;
+  D.if_off = ioff;
+  D.if_code = icode;
+  D.n_if = (int64_t)P.if_off.size() - 1;
+  D.nbr27 = n27;
+  D.gelem = ge;
+  D.recv_total = P.recv_total;
+  void* p = nullptr;
+  SBX_TRY(dalloc(c, &p, 4 * sizeof(unsigned long long)));
+  D.seq = static_cast<unsigned long long*>(p);
+  SBX_TRY(dalloc(c, &p, 4 * sizeof(unsigned int)));
+  D.counter = static_cast<unsigned int*>(p);
+  SBX_TRY(dalloc(c, &p, sizeof(int)));
+  D.status = static_cast<int*>(p);
+  SBX_CUDA(cudaMemsetAsync(D.seq, 0, 4 * sizeof(unsigned long long), c->stream));
+  SBX_CUDA(cudaMemsetAsync(D.counter, 0, 4 * sizeof(unsigned int), c->stream));
+  SBX_CUDA(cudaMemsetAsync(D.status, 0, sizeof(int), c->stream));
+  // peer window (exported over CUDA IPC; own allocation, not via dalloc's list
+  // so it is freed after the peers close their mappings)
+  const size_t wbytes = kWinRecv + sizeof(double) * (size_t)std::max<int64_t>(4 * P.recv_total, 2);
+  SBX_CUDA(cudaMalloc(&c->window, wbytes));
+  SBX_CUDA(cudaMemsetAsync(c->window, 0, wbytes, c->stream));
+  char* wb = static_cast<char*>(c->window);
+  D.flags = reinterpret_cast<unsigned long long*>(wb + kWinFlags);
+  D.mbox = reinterpret_cast<double*>(wb + kWinMbox);
+  D.recv = reinterpret_cast<double*>(wb + kWinRecv);
+  c->recv_base_for_src.assign(kMaxRanks, -1);
+  for (int qi = 0; qi < D.nnbr; ++qi) c->recv_base_for_src[P.nbr[qi]] = P.recv_base[qi];
+  SBX_TRY(ensure_partials(c, std::max<int64_t>(EL, 4096)));
+  c->cg.reset(new CgEngine());
+  SBX_CUDA(cudaStreamSynchronize(c->stream));
+  return SBX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+sbx_status sbx_ctx_create_box_dist(const sbx_box_desc* d, const int32_t* rank_of, int nranks,
+                                   int rank, int device, sbx_ctx** out) {
+  if (!d || !rank_of || !out) {
+    set_error("sbx_ctx_create_box_dist: null argument");
+    return SBX_E_INVALID;
+  }
+  *out = nullptr;
+  if (nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks) {
+    set_error("sbx_ctx_create_box_dist: 1 <= nranks <= 8 and 0 <= rank < nranks");
+    return SBX_E_CONFIG;
+  }
+  const int counts[3] = {d->ex, d->ey, d->ez};
+  for (int q = 0; q < 3; ++q)
+    if (d->periodic[q] && counts[q] < 2) {
+      set_error("sbx_ctx_create_box_dist: periodic directions need >= 2 elements");
+      return SBX_E_CONFIG;
+    }
+  if ((d->degree + 1) % 2 != 0 || d->degree > kMaxTemplN) {
+    set_error("sbx_ctx_create_box_dist: the distributed solver needs an odd degree N <= 15");
+    return SBX_E_CONFIG;
+  }
+  auto plan = std::make_unique<DistPlan>();
+  int rc = build_dist_plan(d->ex, d->ey, d->ez, d->periodic, d->degree, rank_of, nranks, rank,
+                           *plan);
+  if (rc != SBX_OK) return (sbx_status)rc;
+  auto* c = new sbx_ctx();
+  sbx_status st = ctx_init_common(c, device);
+  c->dist = true;
+  c->nranks = nranks;
+  c->rank = rank;
+  c->local_elements = plan->loc_elems;
+  if (st == SBX_OK) st = upload_dist(c, *plan, d);
+  if (st != SBX_OK) {
+    sbx_ctx_destroy(c);
+    return st;
+  }
+  *out = c;
+  return SBX_OK;
+}
+
+size_t sbx_ctx_dist_blob_size(int nranks) {
+  (void)nranks;
+  return sizeof(DistBlob);
+}
+
+sbx_status sbx_ctx_dist_blob(sbx_ctx* c, uint8_t* blob) {
+  SBX_TRY(check_ctx(c));
+  if (!c->dist || !blob) {
+    set_error("sbx_ctx_dist_blob: not a distributed context");
+    return SBX_E_INVALID;
+  }
+  SBX_CUDA(cudaSetDevice(c->device));
+  DistBlob b;
+  std::memset(&b, 0, sizeof(b));
+  SBX_CUDA(cudaIpcGetMemHandle(&b.handle, c->window));
+  b.recv_total = c->dd.recv_total;
+  for (int q = 0; q < kMaxRanks; ++q) b.recv_base_for_src[q] = c->recv_base_for_src[q];
+  std::memcpy(blob, &b, sizeof(b));
+  return SBX_OK;
+}
+
+sbx_status sbx_ctx_dist_connect(sbx_ctx* c, const uint8_t* blobs) {
+  SBX_TRY(check_ctx(c));
+  if (!c->dist || !blobs) {
+    set_error("sbx_ctx_dist_connect: not a distributed context");
+    return SBX_E_INVALID;
+  }
+  SBX_CUDA(cudaSetDevice(c->device));
+  DistDev& D = c->dd;
+  for (int q = 0; q < c->nranks; ++q) {
+    DistBlob b;
+    std::memcpy(&b, blobs + (size_t)q * sizeof(DistBlob), sizeof(DistBlob));
+    char* base = nullptr;
+    if (q == c->rank) {
+      base = static_cast<char*>(c->window);
+    } else {
+      void* p = nullptr;
+      SBX_CUDA(cudaIpcOpenMemHandle(&p, b.handle, cudaIpcMemLazyEnablePeerAccess));
+      c->peer_windows.push_back(p);
+      base = static_cast<char*>(p);
+    }
+    D.pflags[q] = reinterpret_cast<unsigned long long*>(base + kWinFlags);
+    D.pmbox[q] = reinterpret_cast<double*>(base + kWinMbox);
+    D.precv[q] = reinterpret_cast<double*>(base + kWinRecv);
+    D.precv_total[q] = b.recv_total;
+    D.pbase_for_me[q] = b.recv_base_for_src[c->rank];
+    if (q != c->rank) {
+      // a neighbour must have a receive block for me, and I for it
+      bool i_send = false;
+      for (int qi = 0; qi < D.nnbr; ++qi)
+        if (D.nbr[qi] == q) i_send = true;
+      if (i_send != (b.recv_base_for_src[c->rank] >= 0)) {
+        set_error("sbx_ctx_dist_connect: inconsistent exchange plans between ranks");
+        return SBX_E_COMM;
+      }
+    }
+  }
+  c->connected = true;
+  return SBX_OK;
+}
+
+}  // extern "C"

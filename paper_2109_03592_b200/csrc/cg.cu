@@ -26,6 +26,7 @@
 #include "ax_core.cuh"
 #include "ax_tma.cuh"
 #include "cg.cuh"
+#include "dist_kern.cuh"
 #include "sbx_internal.h"
 
 namespace sbx {
@@ -135,6 +136,11 @@ __device__ void CgK1Pol<HAS_DINV, HAS_BM>::finish(const Args& a, double red, dou
   CgScalars* sc = a.sc;
   if (!last_block(&sc->counter[0], flag)) return;
   const double tot = reduce_partials(partials, gridDim.x, 1, 0, sh);
+  if (threadIdx.x == 0 && sc->nranks > 1) {
+    sc->counter[0] = 0;
+    sc->pq_loc = tot;  // summed over ranks by dist_iface_kernel
+    return;
+  }
   if (threadIdx.x == 0) {
     sc->counter[0] = 0;
     sc->pq = tot;
@@ -250,6 +256,13 @@ __device__ __forceinline__ void update_tail(double rz, double rr, double alpha, 
   if (!last_block(&sc->counter[1], is_last)) return;
   const double rz_new = reduce_partials(partials, gridDim.x, 2, 0, red);
   const double rr_new = reduce_partials(partials, gridDim.x, 2, 1, red);
+  if (threadIdx.x == 0 && sc->nranks > 1) {
+    // distributed: rank partials, reduced by dist_cg_scalar_kernel
+    sc->counter[1] = 0;
+    sc->rz_loc = rz_new;
+    sc->rr_loc = rr_new;
+    return;
+  }
   if (threadIdx.x == 0) {
     sc->counter[1] = 0;
     const double rnorm = sqrt(rr_new);
@@ -559,10 +572,11 @@ struct K2Choice {
   static constexpr int SPG = spg();
 };
 
-template <int n, int GROUPS, int SPG>
+template <int n, int GROUPS, int SPG, bool TABLE>
 __global__ void __launch_bounds__(K2Layout<n, GROUPS, SPG>::threads, 1)
     cg_update_tma_kernel(const double* __restrict__ w, double* __restrict__ r,
                          const double* __restrict__ dinv, int64_t E, BoxP bx,
+                         const int32_t* __restrict__ nbr27, const int64_t* __restrict__ gelem,
                          CgScalars* __restrict__ sc, double* __restrict__ partials,
                          double* __restrict__ hist, int64_t hist_cap,
                          cudaGraphConditionalHandle cond, int use_cond) {
@@ -622,40 +636,83 @@ __global__ void __launch_bounds__(K2Layout<n, GROUPS, SPG>::threads, 1)
       // before waiting for the TMA bytes
       Dir X{0, false, false, 0}, Y = X, Z0 = X, ZN = X;
       const double *pw = w, *px = w, *py = w, *pxy = w;
+      // columns (own, x, y, xy) of the element across the k=0 / k=N faces
+      const double *z0p0 = w, *z0p1 = w, *z0p2 = w, *z0p3 = w;
+      const double *zNp0 = w, *zNp1 = w, *zNp2 = w, *zNp3 = w;
+      // TABLE (multi-GPU): a partner on another rank marks an interface group,
+      // already assembled in w by dist_iface_kernel
+      bool rem_xy = false, rem_z0 = false, rem_zN = false;
       if (valid) {
-        const int ee = (int)e;
-        const int cx = ee % bx.ex, cy = (ee / bx.ex) % bx.ey, cz = ee / (bx.ex * bx.ey);
+        const int64_t ge = TABLE ? gelem[e] : e;
+        const int cx = (int)(ge % bx.ex), cy = (int)((ge / bx.ex) % bx.ey);
+        const int cz = (int)(ge / exy);
         X = dir_state(i, N, cx, bx.ex, bx.px, 1);
         Y = dir_state(j, N, cy, bx.ey, bx.py, bx.ex);
         Z0 = dir_state(0, N, cz, bx.ez, bx.pz, exy);
         ZN = dir_state(N, N, cz, bx.ez, bx.pz, exy);
-        pw = w + e * T::n3 + ij;
-        px = w + (e + X.d) * T::n3 + j * n + (N - i);
-        py = w + (e + Y.d) * T::n3 + (N - j) * n + i;
-        pxy = w + (e + X.d + Y.d) * T::n3 + (N - j) * n + (N - i);
+        const int64_t cxo = j * n + (N - i), cyo = (N - j) * n + i, cxyo = (N - j) * n + (N - i);
+        if constexpr (TABLE) {
+          const int32_t* t = nbr27 + e * 27;
+          const int dxi = i == 0 ? 0 : 2, dyi = j == 0 ? 0 : 2;
+          auto id = [&](int xi, int yi, int zi) { return t[xi + 3 * yi + 9 * zi]; };
+          const int32_t lx = X.act ? id(dxi, 1, 1) : 0, ly = Y.act ? id(1, dyi, 1) : 0;
+          const int32_t lxy = (X.act && Y.act) ? id(dxi, dyi, 1) : 0;
+          rem_xy = lx < 0 || ly < 0 || lxy < 0;
+          pw = w + e * T::n3 + ij;
+          px = w + (int64_t)(lx < 0 ? 0 : lx) * T::n3 + cxo;
+          py = w + (int64_t)(ly < 0 ? 0 : ly) * T::n3 + cyo;
+          pxy = w + (int64_t)(lxy < 0 ? 0 : lxy) * T::n3 + cxyo;
+          const int zf[2] = {0, 2};
+          for (int f = 0; f < 2; ++f) {
+            const Dir& Z = f == 0 ? Z0 : ZN;
+            if (!Z.act) continue;
+            const int32_t l0 = id(1, 1, zf[f]);
+            const int32_t l1 = X.act ? id(dxi, 1, zf[f]) : 0;
+            const int32_t l2 = Y.act ? id(1, dyi, zf[f]) : 0;
+            const int32_t l3 = (X.act && Y.act) ? id(dxi, dyi, zf[f]) : 0;
+            const bool rem = rem_xy || l0 < 0 || l1 < 0 || l2 < 0 || l3 < 0;
+            const int64_t ko = (f == 0 ? N : 0) * T::nn;
+            const double* c0 = w + (int64_t)(l0 < 0 ? 0 : l0) * T::n3 + ij + ko;
+            const double* c1 = w + (int64_t)(l1 < 0 ? 0 : l1) * T::n3 + cxo + ko;
+            const double* c2 = w + (int64_t)(l2 < 0 ? 0 : l2) * T::n3 + cyo + ko;
+            const double* c3 = w + (int64_t)(l3 < 0 ? 0 : l3) * T::n3 + cxyo + ko;
+            if (f == 0) {
+              z0p0 = c0, z0p1 = c1, z0p2 = c2, z0p3 = c3, rem_z0 = rem;
+            } else {
+              zNp0 = c0, zNp1 = c1, zNp2 = c2, zNp3 = c3, rem_zN = rem;
+            }
+          }
+        } else {
+          pw = w + e * T::n3 + ij;
+          px = w + (e + X.d) * T::n3 + cxo;
+          py = w + (e + Y.d) * T::n3 + cyo;
+          pxy = w + (e + X.d + Y.d) * T::n3 + cxyo;
+          const int64_t o0 = Z0.d * T::n3 + N * T::nn, oN = ZN.d * T::n3;
+          z0p0 = pw + o0, z0p1 = px + o0, z0p2 = py + o0, z0p3 = pxy + o0;
+          zNp0 = pw + oN, zNp1 = px + oN, zNp2 = py + oN, zNp3 = pxy + oN;
+        }
       }
       const bool axy = X.act && Y.act;
       double wx[n], wy[n], wxy[n];
 #pragma unroll
       for (int k = 0; k < n; ++k) {
-        wx[k] = X.act ? __ldg(px + k * T::nn) : 0.0;
-        wy[k] = Y.act ? __ldg(py + k * T::nn) : 0.0;
-        wxy[k] = axy ? __ldg(pxy + k * T::nn) : 0.0;
+        const bool rk = k == 0 ? rem_z0 : (k == N ? rem_zN : rem_xy);
+        wx[k] = (X.act && !rk) ? __ldg(px + k * T::nn) : 0.0;
+        wy[k] = (Y.act && !rk) ? __ldg(py + k * T::nn) : 0.0;
+        wxy[k] = (axy && !rk) ? __ldg(pxy + k * T::nn) : 0.0;
       }
       double z0c0 = 0, z0c1 = 0, z0c2 = 0, z0c3 = 0, zNc0 = 0, zNc1 = 0, zNc2 = 0, zNc3 = 0;
-      if (Z0.act) {
-        const int64_t o = Z0.d * T::n3 + N * T::nn;
-        z0c0 = __ldg(pw + o);
-        if (X.act) z0c1 = __ldg(px + o);
-        if (Y.act) z0c2 = __ldg(py + o);
-        if (axy) z0c3 = __ldg(pxy + o);
+      if (Z0.act && !rem_z0) {
+        z0c0 = __ldg(z0p0);
+        if (X.act) z0c1 = __ldg(z0p1);
+        if (Y.act) z0c2 = __ldg(z0p2);
+        if (axy) z0c3 = __ldg(z0p3);
       }
-      if (ZN.act) {
-        const int64_t o = ZN.d * T::n3;
-        zNc0 = __ldg(pw + o);
-        if (X.act) zNc1 = __ldg(px + o);
-        if (Y.act) zNc2 = __ldg(py + o);
-        if (axy) zNc3 = __ldg(pxy + o);
+      if (ZN.act && !rem_zN) {
+        zNc0 = __ldg(zNp0);
+        if (X.act) zNc1 = __ldg(zNp1);
+        if (Y.act) zNc2 = __ldg(zNp2);
+        if (axy) zNc3 = __ldg(zNp3);
       }
       mbar_wait(&full[s], (uint32_t)((m / S) & 1));
       const int shift = (int)(((e - sl) * T::n3) & 1);
@@ -671,9 +728,10 @@ __global__ void __launch_bounds__(K2Layout<n, GROUPS, SPG>::threads, 1)
           const double dv = dinv ? slot[2 * L::V_D + k * T::nn] : 1.0;
           const Dir Z = k == 0 ? Z0 : (k == N ? ZN : Dir{0, false, false, 0});
           double q;
+          const bool rk = k == 0 ? rem_z0 : (k == N ? rem_zN : rem_xy);
           if (mxy || ((k == 0 || k == N) && Z.msk)) {
             q = 0.0;
-          } else if (cxy + Z.act == 0) {
+          } else if (cxy + Z.act == 0 || rk) {
             q = wo;
           } else {
             double sum = 0.0;
@@ -938,22 +996,24 @@ cudaError_t launch_k2(const OpDev& op, const double* w, double* r, const double*
       aligned16(r) && aligned16(dinv)) {
     using Ch = K2Choice<n>;
     using L = K2Layout<n, Ch::GROUPS, Ch::SPG>;
-    auto kern = cg_update_tma_kernel<n, Ch::GROUPS, Ch::SPG>;
-    static bool attr_set[64] = {};
+    auto kern = op.table ? cg_update_tma_kernel<n, Ch::GROUPS, Ch::SPG, true>
+                         : cg_update_tma_kernel<n, Ch::GROUPS, Ch::SPG, false>;
+    static bool attr_set[2][64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
-    if (!attr_set[dev & 63]) {
+    if (!attr_set[op.table][dev & 63]) {
       cudaError_t err =
           cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::smem);
       if (err != cudaSuccess) return err;
-      attr_set[dev & 63] = true;
+      attr_set[op.table][dev & 63] = true;
     }
     const int64_t NG = (op.E + TmaGeom<n>::EPG - 1) / TmaGeom<n>::EPG;
     int64_t grid = num_sms(dev);
     if (grid > NG) grid = NG;
     BoxP bx{op.ex, op.ey, op.ez, op.per[0], op.per[1], op.per[2], 0};
-    kern<<<(unsigned)grid, L::threads, L::smem, s>>>(w, r, dinv, op.E, bx, sc, partials, hist,
-                                                     hist_cap, cond, use_cond);
+    kern<<<(unsigned)grid, L::threads, L::smem, s>>>(w, r, dinv, op.E, bx, op.nbr27, op.gelem,
+                                                     sc, partials, hist, hist_cap, cond,
+                                                     use_cond);
     return cudaGetLastError();
   }
   if (op.box && use_flat) {
@@ -1055,7 +1115,46 @@ cudaError_t k2(const OpDev& op, const double* w, double* r, const double* dinv, 
   return err;
 }
 
+unsigned blocks_for(int64_t work, int threads, int64_t cap) {
+  int64_t b = (work + threads - 1) / threads;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (unsigned)b;
+}
+
+// One distributed CG iteration after K1: halo + p'Ap out, interface groups
+// and alpha in, K2, r'z/r'r all-reduce and the scalar step.
+cudaError_t dist_iteration_tail(const OpDev& op, const DistDev& D, double* w, double* r,
+                                const double* dinv, CgScalars* sc, double* partials,
+                                double* hist, int64_t hist_cap, cudaGraphConditionalHandle cond,
+                                int use_cond, cudaStream_t s) {
+  dist_put_kernel<<<blocks_for(D.send_off[D.nnbr], 256, 296), 256, 0, s>>>(D, 0, 0, w,
+                                                                           &sc->pq_loc, 1);
+  dist_iface_kernel<<<blocks_for(D.n_if, 256, 592), 256, 0, s>>>(D, 0, 0, w, 1, sc);
+  cudaError_t err = k2(op, w, r, dinv, sc, partials, hist, hist_cap, cond, 0, s);
+  if (err != cudaSuccess) return err;
+  dist_cg_scalar_kernel<<<1, 32, 0, s>>>(D, sc, hist, hist_cap, cond, use_cond);
+  return cudaGetLastError();
+}
+
 }  // namespace
+
+cudaError_t launch_dist_gs(const OpDev& op, const DistDev& D, double* f, bool apply_mask,
+                           cudaStream_t s) {
+  dist_put_kernel<<<blocks_for(D.send_off[D.nnbr], 256, 296), 256, 0, s>>>(D, 2, 1, f, nullptr,
+                                                                           0);
+  dist_iface_kernel<<<blocks_for(D.n_if, 256, 592), 256, 0, s>>>(D, 2, 1, f, apply_mask ? 1 : 0,
+                                                                 nullptr);
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return err;
+  return launch_gs(op, f, apply_mask, s);
+}
+
+cudaError_t launch_dist_allreduce(const DistDev& D, int phase, const double* in, double* out,
+                                  int count, cudaStream_t s) {
+  dist_allreduce_kernel<<<1, 32, 0, s>>>(D, phase, in, out, count);
+  return cudaGetLastError();
+}
 
 #define CG_CUDA(call)                                                       \
   do {                                                                      \
@@ -1138,8 +1237,11 @@ int CgEngine::build_graph(const CgRun& run) {
                                         cudaStreamCaptureModeRelaxed));
   cudaError_t e1 = k1(op, r_, run.dinv, p_, run.x, w_, run.h1, run.h2, sc_, partials_,
                       run.stream);
-  cudaError_t e2 = k2(op, w_, r_, run.dinv, sc_, partials_, hist_, hist_len_, handle, 1,
-                      run.stream);
+  cudaError_t e2 =
+      run.dist ? dist_iteration_tail(op, *run.dist, w_, r_, run.dinv, sc_, partials_, hist_,
+                                     hist_len_, handle, 1, run.stream)
+               : k2(op, w_, r_, run.dinv, sc_, partials_, hist_, hist_len_, handle, 1,
+                    run.stream);
   cudaGraph_t captured = nullptr;
   cudaError_t e3 = cudaStreamEndCapture(run.stream, &captured);
   CG_CUDA(e1);
@@ -1163,7 +1265,11 @@ int CgEngine::run_timed_loop(const CgRun& run) {
     CG_CUDA(cudaEventRecord(ev[0], run.stream));
     CG_CUDA(k1(op, r_, run.dinv, p_, run.x, w_, run.h1, run.h2, sc_, partials_, run.stream));
     CG_CUDA(cudaEventRecord(ev[1], run.stream));
-    CG_CUDA(k2(op, w_, r_, run.dinv, sc_, partials_, hist_, hist_len_, none, 0, run.stream));
+    if (run.dist)
+      CG_CUDA(dist_iteration_tail(op, *run.dist, w_, r_, run.dinv, sc_, partials_, hist_,
+                                  hist_len_, none, 0, run.stream));
+    else
+      CG_CUDA(k2(op, w_, r_, run.dinv, sc_, partials_, hist_, hist_len_, none, 0, run.stream));
     CG_CUDA(cudaEventRecord(ev[2], run.stream));
     CG_CUDA(cudaMemcpyAsync(hsc_, sc_, sizeof(CgScalars), cudaMemcpyDeviceToHost, run.stream));
     CG_CUDA(cudaEventSynchronize(ev[2]));
@@ -1187,7 +1293,10 @@ int CgEngine::solve(const CgRun& run, sbx_pcg_result* res) {
   if (ensure(run) != SBX_OK) return SBX_E_CUDA;
   cudaStream_t s = run.stream;
   const int64_t N = op.nodes;
+  const DistDev* D = run.dist;
   // right-hand side must be continuous and masked for the fused p'Ap
+  // (checked on this rank's shared groups; cross-rank continuity is the
+  // caller's contract in the distributed case)
   CG_CUDA(cudaMemsetAsync(flag_, 0, sizeof(int), s));
   if (op.nB > 0)
     cg_check_rhs_kernel<<<(unsigned)((op.nB + 255) / 256), 256, 0, s>>>(op.b_off, op.b_idx,
@@ -1197,12 +1306,35 @@ int CgEngine::solve(const CgRun& run, sbx_pcg_result* res) {
   CG_CUDA(cudaMemsetAsync(flag_ + 1, 0, sizeof(int), s));
   cg_any_nonzero_kernel<<<(unsigned)std::min<int64_t>((N + 255) / 256, 148 * 8), 256, 0, s>>>(
       N, run.x, flag_ + 1);
-  int hnz = 0;
-  CG_CUDA(cudaMemcpyAsync(&hnz, flag_ + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+  int hflags[2] = {0, 0};
+  CG_CUDA(cudaMemcpyAsync(hflags, flag_, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
   CG_CUDA(cudaStreamSynchronize(s));
+  int hnz = hflags[1];
+  if (D) {
+    // both decisions are global: any rank nonzero -> apply everywhere; any
+    // rank with a non-continuous rhs -> error everywhere (no exact fallback)
+    double loc[2] = {hnz ? 1.0 : 0.0, hflags[0] ? 1.0 : 0.0};
+    CG_CUDA(cudaMemcpyAsync(init_ + 4, loc, sizeof(loc), cudaMemcpyHostToDevice, s));
+    CG_CUDA(launch_dist_allreduce(*D, 3, init_ + 4, init_ + 6, 2, s));
+    double tot[2] = {0.0, 0.0};
+    CG_CUDA(cudaMemcpyAsync(tot, init_ + 6, sizeof(tot), cudaMemcpyDeviceToHost, s));
+    CG_CUDA(cudaStreamSynchronize(s));
+    if (!(tot[0] >= 0.0)) {
+      err_ = "multi-GPU exchange timed out";
+      return SBX_E_COMM;
+    }
+    if (tot[1] > 0.0) {
+      err_ = "distributed pcg needs a continuous, masked right-hand side";
+      return SBX_E_SHAPE;
+    }
+    hnz = tot[0] > 0.0;
+  }
   if (hnz) {
     CG_CUDA(launch_axhelm(op, run.x, w_, run.h1, run.h2, false, false, s));
-    CG_CUDA(launch_gs(op, w_, true, s));
+    if (D)
+      CG_CUDA(launch_dist_gs(op, *D, w_, true, s));
+    else
+      CG_CUDA(launch_gs(op, w_, true, s));
   }
   const double* dinv = run.dinv;
   {
@@ -1214,12 +1346,15 @@ int CgEngine::solve(const CgRun& run, sbx_pcg_result* res) {
                                                     partials_, &sc_->counter[2], init_);
     CG_CUDA(cudaGetLastError());
   }
+  if (D) CG_CUDA(launch_dist_allreduce(*D, 3, init_, init_, 4, s));
   double hinit[4];
-  int hflag = 0;
   CG_CUDA(cudaMemcpyAsync(hinit, init_, sizeof(hinit), cudaMemcpyDeviceToHost, s));
-  CG_CUDA(cudaMemcpyAsync(&hflag, flag_, sizeof(int), cudaMemcpyDeviceToHost, s));
   CG_CUDA(cudaStreamSynchronize(s));
-  if (hflag) return kCgFallback;
+  if (!D && hflags[0]) return kCgFallback;
+  if (D && !(hinit[0] == hinit[0])) {
+    err_ = "multi-GPU exchange timed out";
+    return SBX_E_COMM;
+  }
   const double bb = hinit[0], bmb = hinit[1], rz = hinit[2], rr = hinit[3];
   res->history_length = 0;
   if (bb == 0.0) {
@@ -1245,6 +1380,7 @@ int CgEngine::solve(const CgRun& run, sbx_pcg_result* res) {
   h.first = 1;
   h.done = 0;
   h.err_it = -1;
+  h.nranks = D ? D->nranks : 1;
   const bool conv0 = rel0 <= run.tol && relp0 <= run.tol;
   if (conv0) {
     h.converged = 1;
@@ -1284,6 +1420,10 @@ int CgEngine::solve(const CgRun& run, sbx_pcg_result* res) {
     res->error_iteration = o.err_it;
     res->history_length = (int64_t)o.it + 1;
     return o.status;
+  }
+  if (o.status == 8) {
+    err_ = "multi-GPU exchange timed out (a peer rank stopped responding)";
+    return SBX_E_COMM;
   }
   return SBX_OK;
 }

@@ -25,6 +25,7 @@ struct CgRun {
   int64_t history_capacity = 0;
   bool interior_clean = false;
   bool timing = false;
+  const DistDev* dist = nullptr;  // multi-GPU exchange state, or null
 };
 
 // Returned by solve() when the FAST schedule's preconditions do not hold

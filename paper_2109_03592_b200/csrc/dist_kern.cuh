@@ -1,0 +1,232 @@
+// Peer-window exchange kernels for the distributed PCG (included by cg.cu).
+//
+// A sender stores raw copy values straight into the receiver's window over
+// NVLink (plain st.global on IPC-mapped peer pointers), fences at system
+// scope, and releases a per-(phase, source) sequence flag; the receiver
+// acquires the flags of all ranks, then reads its window.  Scalars travel in
+// per-source mailboxes and are summed in rank order, so every rank computes
+// bit-identical CG scalars.  Waits are bounded (kSpinTimeoutNs) and report a
+// communication error instead of hanging.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.cuh"
+
+namespace sbx {
+namespace {
+
+constexpr unsigned long long kSpinTimeoutNs = 20ull * 1000 * 1000 * 1000;
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
+  return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+
+// Wait until every other rank released `phase` with sequence >= expected.
+__device__ bool dist_wait_all(const DistDev& D, int phase, unsigned long long expected) {
+  const unsigned long long t0 = globaltimer();
+  for (int q = 0; q < D.nranks; ++q) {
+    if (q == D.rank) continue;
+    const unsigned long long* f = D.flags + phase * kMaxRanks + q;
+    while (ld_acquire_sys(f) < expected) {
+      if (globaltimer() - t0 > kSpinTimeoutNs) return false;
+      __nanosleep(64);
+    }
+  }
+  return true;
+}
+
+// Stores this rank's send values (w at the send lists) into the neighbours'
+// receive buffers, its scalars into every rank's mailbox, then releases the
+// phase flag on every rank.  slot: receive-buffer slot (0 loop, 1 standalone).
+__global__ void dist_put_kernel(DistDev D, int phase, int slot, const double* __restrict__ w,
+                                const double* __restrict__ scal, int nscal) {
+  __shared__ bool last;
+  const unsigned long long s = ld_volatile_u64(D.seq + phase);
+  const int64_t par = (int64_t)((s + 1) & 1);
+  const int64_t total = D.send_off[D.nnbr];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int qi = 0;
+    while (i >= D.send_off[qi + 1]) ++qi;
+    const int q = D.nbr[qi];
+    double* dst = D.precv[q] + (slot * 2 + par) * D.precv_total[q] + D.pbase_for_me[q] +
+                  (i - D.send_off[qi]);
+    *dst = w[D.send_idx[i]];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(D.counter + phase, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last || threadIdx.x != 0) return;
+  __threadfence_system();
+  D.counter[phase] = 0;
+  for (int q = 0; q < D.nranks; ++q)
+    for (int c = 0; c < nscal; ++c)
+      D.pmbox[q][mbox_index(phase, (int)par, D.rank, c)] = scal[c];
+  __threadfence_system();
+  for (int q = 0; q < D.nranks; ++q)
+    if (q != D.rank) st_release_sys(D.pflags[q] + phase * kMaxRanks + D.rank, s + 1);
+  D.seq[phase] = s + 1;
+}
+
+// Rank-order sum of mailbox entry c of `phase`.
+__device__ __forceinline__ double mbox_sum(const DistDev& D, int phase, int par, int c) {
+  double v = 0.0;
+  for (int q = 0; q < D.nranks; ++q) {
+    const volatile double* m = D.mbox + mbox_index(phase, par, q, c);
+    v += *m;
+  }
+  return v;
+}
+
+// Interface groups: wait for the halo, sum every copy in canonical order
+// (local copies from f, remote ones from the receive buffer) and write the sum
+// to the local copies (s*0 for masked ones when apply_mask).  In the CG loop
+// (sc != null) block 0 also forms alpha = rz / sum_q pq_q and tests breakdown.
+__global__ void dist_iface_kernel(DistDev D, int phase, int slot, double* __restrict__ f,
+                                  int apply_mask, CgScalars* __restrict__ sc) {
+  __shared__ bool ok;
+  if (sc && sc->done) return;
+  if (threadIdx.x == 0) {
+    ok = dist_wait_all(D, phase, ld_volatile_u64(D.seq + phase));
+    if (!ok) *D.status = 1;
+  }
+  __syncthreads();
+  if (!ok) {
+    if (sc && blockIdx.x == 0 && threadIdx.x == 0) {
+      sc->status = 8;
+      sc->done = 1;
+    }
+    return;
+  }
+  if (sc && blockIdx.x == 0 && threadIdx.x == 0) {
+    const double pq = mbox_sum(D, phase, (int)(ld_volatile_u64(D.seq + phase) & 1), 0);
+    sc->pq = pq;
+    if (!isfinite(pq) || pq <= 0.0) {
+      sc->status = 5;
+      sc->err_it = sc->it;
+      sc->done = 1;
+    } else {
+      sc->alpha = sc->rz / pq;
+    }
+  }
+  const int64_t par = (int64_t)(ld_volatile_u64(D.seq + phase) & 1);
+  const double* rb = D.recv + (slot * 2 + par) * D.recv_total;
+  const int64_t NL = D.nodes_local;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < D.n_if;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int lo = D.if_off[g], hi = D.if_off[g + 1];
+    double sum = 0.0;
+    for (int c = lo; c < hi; ++c) {
+      const int32_t code = D.if_code[c];
+      sum += code >= NL ? __ldcv(rb + (code - NL)) : f[code < 0 ? ~code : code];
+    }
+    for (int c = lo; c < hi; ++c) {
+      const int32_t code = D.if_code[c];
+      if (code >= NL) continue;
+      if (code >= 0)
+        f[code] = sum;
+      else
+        f[~code] = apply_mask ? __dmul_rn(sum, 0.0) : sum;
+    }
+  }
+}
+
+// Scalar all-reduce (rank order) of `count` doubles; one thread.
+__global__ void dist_allreduce_kernel(DistDev D, int phase, const double* __restrict__ in,
+                                      double* __restrict__ out, int count) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const unsigned long long s = ld_volatile_u64(D.seq + phase);
+  for (int q = 0; q < D.nranks; ++q)
+    for (int c = 0; c < count; ++c)
+      D.pmbox[q][mbox_index(phase, (int)((s + 1) & 1), D.rank, c)] = in[c];
+  __threadfence_system();
+  for (int q = 0; q < D.nranks; ++q)
+    if (q != D.rank) st_release_sys(D.pflags[q] + phase * kMaxRanks + D.rank, s + 1);
+  D.seq[phase] = s + 1;
+  if (!dist_wait_all(D, phase, s + 1)) {
+    *D.status = 1;
+    for (int c = 0; c < count; ++c) out[c] = nan("");
+    return;
+  }
+  for (int c = 0; c < count; ++c) out[c] = mbox_sum(D, phase, (int)((s + 1) & 1), c);
+}
+
+// End of a distributed CG iteration: all-reduce r'z, r'r (phase 1), then the
+// scalar logic of update_tail (beta, history, convergence, NaN) and the WHILE
+// condition.
+__global__ void dist_cg_scalar_kernel(DistDev D, CgScalars* __restrict__ sc,
+                                      double* __restrict__ hist, int64_t hist_cap,
+                                      cudaGraphConditionalHandle cond, int use_cond) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (sc->done) {
+    if (use_cond) cudaGraphSetConditional(cond, 0);
+    return;
+  }
+  const int phase = 1;
+  const unsigned long long s = ld_volatile_u64(D.seq + phase);
+  const double mine[2] = {sc->rz_loc, sc->rr_loc};
+  for (int q = 0; q < D.nranks; ++q)
+    for (int c = 0; c < 2; ++c)
+      D.pmbox[q][mbox_index(phase, (int)((s + 1) & 1), D.rank, c)] = mine[c];
+  __threadfence_system();
+  for (int q = 0; q < D.nranks; ++q)
+    if (q != D.rank) st_release_sys(D.pflags[q] + phase * kMaxRanks + D.rank, s + 1);
+  D.seq[phase] = s + 1;
+  if (!dist_wait_all(D, phase, s + 1)) {
+    *D.status = 1;
+    sc->status = 8;
+    sc->done = 1;
+    if (use_cond) cudaGraphSetConditional(cond, 0);
+    return;
+  }
+  const double rz_new = mbox_sum(D, phase, (int)((s + 1) & 1), 0);
+  const double rr_new = mbox_sum(D, phase, (int)((s + 1) & 1), 1);
+  const double rnorm = sqrt(rr_new);
+  const int it = sc->it;
+  if (!isfinite(rnorm) || !isfinite(rz_new)) {
+    sc->status = 6;
+    sc->err_it = it;
+    sc->done = 1;
+  } else {
+    const double rel = rnorm / sc->bnorm;
+    if (hist && it + 1 < hist_cap) hist[it + 1] = rel;
+    sc->it = it + 1;
+    sc->beta = rz_new / sc->rz;
+    sc->rz = rz_new;
+    sc->rr = rr_new;
+    sc->alpha_prev = sc->alpha;
+    sc->first = 0;
+    sc->rel = rel;
+    sc->relp = sc->bmb > 0.0 ? sqrt(fmax(rz_new, 0.0) / sc->bmb) : 0.0;
+    if (sc->rel <= sc->tol && sc->relp <= sc->tol) {
+      sc->converged = 1;
+      sc->done = 1;
+    } else if (sc->it >= sc->max_it) {
+      sc->done = 1;
+    }
+  }
+  if (use_cond) cudaGraphSetConditional(cond, sc->done ? 0 : 1);
+}
+
+}  // namespace
+}  // namespace sbx

@@ -31,8 +31,13 @@ struct OpDev {
   // gather-scatter that derives every copy from the cell lattice instead of
   // reading the CSR.  Requires count_d >= 2 in every periodic direction.
   bool box = false;
-  int ex = 0, ey = 0, ez = 0;
+  int ex = 0, ey = 0, ez = 0;  // GLOBAL box dims
   int per[3] = {0, 0, 0};
+  // multi-GPU: this rank's elements are a subset; partners via the
+  // 27-neighbourhood table (local id / -1 outside / -2 on another rank)
+  bool table = false;
+  const int32_t* nbr27 = nullptr;
+  const int64_t* gelem = nullptr;
 };
 
 // Device-resident CG scalars for the fused (FAST) solver.
@@ -54,9 +59,60 @@ struct CgScalars {
   int32_t converged;
   int32_t status;   // 0 ok, 5 breakdown, 6 NaN
   int32_t err_it;
-  int32_t pad;
+  int32_t nranks;   // > 1: distributed (rank-local partials, exchange kernels)
   uint32_t counter[4];  // last-block-done tickets
+  double pq_loc, rz_loc, rr_loc;  // this rank's partials (distributed)
 };
+
+// ---- multi-GPU peer windows ------------------------------------------------
+constexpr int kMaxRanks = 8;
+// Window layout (bytes): flags [4 phases][kMaxRanks] u64 at 0, mailboxes
+// [4 phases][2 parities][kMaxRanks][4] f64 at 256, receive buffers
+// [2 slots][2 parities][recv_total] f64 at 2304.  Phases: 0 halo+p'Ap in the
+// CG loop, 1 r'z/r'r, 2 standalone gather-scatter halo, 3 setup reductions.
+// Parity = sequence number & 1: a peer can run at most one use of a phase
+// ahead (it needs this rank's flag of the previous use), so double buffering
+// makes every read race-free.
+constexpr size_t kWinFlags = 0, kWinMbox = 256, kWinRecv = 2304;
+
+__host__ __device__ constexpr int mbox_index(int phase, int par, int src, int c) {
+  return ((phase * 2 + par) * kMaxRanks + src) * 4 + c;
+}
+
+struct DistDev {
+  int nranks = 1, rank = 0;
+  int64_t nodes_local = 0;
+  unsigned long long* flags = nullptr;  // my window
+  double* mbox = nullptr;
+  double* recv = nullptr;
+  int64_t recv_total = 0;
+  unsigned long long* pflags[kMaxRanks] = {};  // peer windows (own rank: mine)
+  double* pmbox[kMaxRanks] = {};
+  double* precv[kMaxRanks] = {};
+  int64_t precv_total[kMaxRanks] = {};
+  int64_t pbase_for_me[kMaxRanks] = {};  // my block's offset in peer q's receive buffer
+  int nnbr = 0;
+  int nbr[kMaxRanks] = {};
+  int64_t send_off[kMaxRanks + 1] = {};
+  const int32_t* send_idx = nullptr;
+  int64_t n_if = 0;
+  const int32_t* if_off = nullptr;
+  const int32_t* if_code = nullptr;
+  const int32_t* nbr27 = nullptr;  // local elements' 27-neighbourhood
+  const int64_t* gelem = nullptr;  // global element id of each local element
+  unsigned long long* seq = nullptr;  // device [4]
+  unsigned int* counter = nullptr;    // device [4]
+  int* status = nullptr;              // device: 1 on exchange timeout
+};
+
+// distributed gather-scatter of a local field (halo exchange over the peer
+// windows, interface groups summed in canonical order, then the local
+// boundary CSR); apply_mask as in launch_gs
+cudaError_t launch_dist_gs(const OpDev& op, const DistDev& D, double* f, bool apply_mask,
+                           cudaStream_t s);
+// sum of up to 4 doubles over all ranks, in rank order (device in/out)
+cudaError_t launch_dist_allreduce(const DistDev& D, int phase, const double* in, double* out,
+                                  int count, cudaStream_t s);
 
 // ---- standalone operators (ops.cu) ----------------------------------------
 cudaError_t launch_axhelm(const OpDev& op, const double* u, double* w, double h1, double h2,

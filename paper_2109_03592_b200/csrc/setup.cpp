@@ -19,6 +19,7 @@
 #include <thread>
 #include <vector>
 
+#include "lattice.h"
 #include "sbx_internal.h"
 
 namespace sbx {
@@ -246,50 +247,6 @@ int geometric_factors(int64_t E, int degree, const double* corners, double* cons
 // the Cartesian product of those options; groups are enumerated in lattice
 // (= gid) order and copies sorted by local index, which reproduces the
 // reference's sort on (gid, local index) (gather.cpp:48-70) exactly.
-namespace {
-struct AxisOpts {
-  int count = 1;
-  int64_t cell[2];
-  int loc[2];
-};
-
-struct Lattice {
-  int counts[3];
-  int N;
-  bool per[3];
-  int64_t gdim[3];
-
-  AxisOpts opts(int d, int64_t g) const {
-    AxisOpts o;
-    const int64_t span = static_cast<int64_t>(counts[d]) * N;
-    if (g % N != 0) {
-      o.count = 1;
-      o.cell[0] = g / N;
-      o.loc[0] = static_cast<int>(g % N);
-      return o;
-    }
-    o.count = 0;
-    if (per[d]) {
-      // g == c*N: loc 0 of cell c and loc N of cell c-1 (wrapping)
-      o.cell[o.count] = g / N;
-      o.loc[o.count++] = 0;
-      o.cell[o.count] = (g / N - 1 + counts[d]) % counts[d];
-      o.loc[o.count++] = N;
-    } else {
-      if (g > 0) {
-        o.cell[o.count] = g / N - 1;
-        o.loc[o.count++] = N;
-      }
-      if (g < span) {
-        o.cell[o.count] = g / N;
-        o.loc[o.count++] = 0;
-      }
-    }
-    return o;
-  }
-};
-}  // namespace
-
 int gather_scatter(int ex, int ey, int ez, const int* periodic, int degree, int64_t* gid,
                    int64_t* offsets, int64_t* group_nodes, int32_t* mult, double* inv_mult,
                    int64_t* global_count) {
