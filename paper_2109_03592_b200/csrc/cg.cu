@@ -729,38 +729,34 @@ __global__ void __launch_bounds__(K2Layout<n, GROUPS, SPG>::threads, 1)
           const Dir Z = k == 0 ? Z0 : (k == N ? ZN : Dir{0, false, false, 0});
           double q;
           const bool rk = k == 0 ? rem_z0 : (k == N ? rem_zN : rem_xy);
-          if (mxy || ((k == 0 || k == N) && Z.msk)) {
-            q = 0.0;
-          } else if (cxy + Z.act == 0 || rk) {
-            q = wo;
-          } else {
-            double sum = 0.0;
+          const bool msk = mxy || ((k == 0 || k == N) && Z.msk);
+          // Branch-free canonical sum over the 8 copy slots (z-side outer, y,
+          // x inner; in each direction the smaller cell first).  Inactive
+          // slots add +0.0; every copy of a node runs the identical sequence,
+          // so all copies get the same bits.  Interface nodes (rk) were
+          // assembled by dist_iface_kernel: own value only.
+          const bool ax = X.act && !rk, ay = Y.act && !rk, az = Z.act && !rk;
+          const bool lo = (k == 0);
+          const double zc0 = lo ? z0c0 : zNc0, zc1 = lo ? z0c1 : zNc1;
+          const double zc2 = lo ? z0c2 : zNc2, zc3 = lo ? z0c3 : zNc3;
+          double sum = 0.0;
 #pragma unroll
-            for (int zs = 0; zs < 2; ++zs) {
-              if (zs == 1 && !Z.act) break;
-              const bool zn = Z.act && ((zs == 0) == Z.nfirst);
+          for (int zs = 0; zs < 2; ++zs) {
 #pragma unroll
-              for (int ys = 0; ys < 2; ++ys) {
-                if (ys == 1 && !Y.act) break;
-                const bool yn = Y.act && ((ys == 0) == Y.nfirst);
+            for (int ys = 0; ys < 2; ++ys) {
 #pragma unroll
-                for (int xs = 0; xs < 2; ++xs) {
-                  if (xs == 1 && !X.act) break;
-                  const bool xn = X.act && ((xs == 0) == X.nfirst);
-                  double v;
-                  if (zn) {
-                    const bool lo = (k == 0);
-                    v = yn ? (xn ? (lo ? z0c3 : zNc3) : (lo ? z0c2 : zNc2))
-                           : (xn ? (lo ? z0c1 : zNc1) : (lo ? z0c0 : zNc0));
-                  } else {
-                    v = yn ? (xn ? wxy[k] : wy[k]) : (xn ? wx[k] : wo);
-                  }
-                  sum += v;
-                }
+              for (int xs = 0; xs < 2; ++xs) {
+                const bool on = (zs == 0 || az) && (ys == 0 || ay) && (xs == 0 || ax);
+                const bool zn = az && ((zs == 0) == Z.nfirst);
+                const bool yn = ay && ((ys == 0) == Y.nfirst);
+                const bool xn = ax && ((xs == 0) == X.nfirst);
+                const double vp = yn ? (xn ? wxy[k] : wy[k]) : (xn ? wx[k] : wo);
+                const double vz = yn ? (xn ? zc3 : zc2) : (xn ? zc1 : zc0);
+                sum += on ? (zn ? vz : vp) : 0.0;
               }
             }
-            q = sum;
           }
+          q = msk ? 0.0 : sum;
           const int cnt = cxy + Z.act;
           const double wgt = cnt == 0 ? 1.0 : cnt == 1 ? 0.5 : cnt == 2 ? 0.25 : 0.125;
           const double rv = fma(-alpha, q, ro);
