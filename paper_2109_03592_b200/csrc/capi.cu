@@ -1015,6 +1015,15 @@ sbx_status upload_dist(sbx_ctx* c, const DistPlan& P, const sbx_box_desc* d) {
   D.send_idx = dsidx;
   D.if_off = ioff;
   D.if_code = icode;
+  int32_t *eo = nullptr, *en = nullptr, *eq = nullptr, *ep = nullptr;
+  SBX_TRY(dupload(c, &eo, P.esend_off.data(), (int64_t)P.esend_off.size()));
+  SBX_TRY(dupload(c, &en, P.esend_node.data(), (int64_t)P.esend_node.size()));
+  SBX_TRY(dupload(c, &eq, P.esend_q.data(), (int64_t)P.esend_q.size()));
+  SBX_TRY(dupload(c, &ep, P.esend_pos.data(), (int64_t)P.esend_pos.size()));
+  D.esend_off = eo;
+  D.esend_node = en;
+  D.esend_q = eq;
+  D.esend_pos = ep;
   D.n_if = (int64_t)P.if_off.size() - 1;
   D.nbr27 = n27;
   D.gelem = ge;
@@ -1147,6 +1156,12 @@ sbx_status sbx_ctx_dist_connect(sbx_ctx* c, const uint8_t* blobs) {
       }
     }
   }
+  // device copy of the exchange state for the fused kernels (K1 epilogue
+  // sends, K2 scalar step)
+  void* p = nullptr;
+  SBX_TRY(dalloc(c, &p, sizeof(DistDev)));
+  SBX_CUDA(cudaMemcpy(p, &c->dd, sizeof(DistDev), cudaMemcpyHostToDevice));
+  c->op.dd = static_cast<const DistDev*>(p);
   c->connected = true;
   return SBX_OK;
 }

@@ -93,15 +93,27 @@ struct CgK1Pol {
     const double* bm;
     double h2;
     CgScalars* sc;
+    const DistDev* dd;  // multi-GPU: interface values go out from the epilogue
     double beta, ap;
     int first;
+    int par;  // receive-buffer parity of this iteration's halo (phase 0)
   };
   __device__ static bool init(Args& a) {
     if (a.sc->done) return false;
     a.first = a.sc->first;
     a.beta = a.sc->beta;
     a.ap = a.sc->alpha_prev;
+    a.par = a.dd ? (int)((*(const volatile unsigned long long*)a.dd->seq + 1) & 1) : 0;
     return true;
+  }
+  // after the element(s) of a step are written: put their interface values on
+  // the wire (group-uniform; no-op on a single GPU)
+  __device__ static void element_done(const Args& a, int64_t e0, int cnt, int n3, int lt,
+                                      int tg, int bar) {
+    if (!a.dd) return;
+    if (a.dd->esend_off[e0] == a.dd->esend_off[e0 + cnt]) return;
+    named_bar_sync(bar, tg);  // w of the step visible to the whole group
+    dist_send_elements(a.dd, a.par, a.w, e0, cnt, n3, lt, tg);
   }
   __device__ static const double* vec(const Args& a, int q) {
     return q == 0 ? a.r : q == 1 ? a.p : q == 2 ? a.x : (HAS_DINV && q == QD) ? a.dinv : a.bm;
@@ -139,6 +151,9 @@ __device__ void CgK1Pol<HAS_DINV, HAS_BM>::finish(const Args& a, double red, dou
   if (threadIdx.x == 0 && sc->nranks > 1) {
     sc->counter[0] = 0;
     sc->pq_loc = tot;  // summed over ranks by dist_iface_kernel
+    // every CTA fenced its interface stores before its ticket: release the
+    // halo and this rank's p'Ap to all ranks
+    if (a.dd) dist_release_phase0(*a.dd, tot);
     return;
   }
   if (threadIdx.x == 0) {
@@ -245,7 +260,8 @@ __device__ __forceinline__ void update_tail(double rz, double rr, double alpha, 
                                             bool* is_last, CgScalars* __restrict__ sc,
                                             double* __restrict__ partials,
                                             double* __restrict__ hist, int64_t hist_cap,
-                                            cudaGraphConditionalHandle cond, int use_cond) {
+                                            cudaGraphConditionalHandle cond, int use_cond,
+                                            const DistDev* dd = nullptr) {
   rz = cta_sum(rz, red);
   const double rz_b = rz;
   rr = cta_sum(rr, red);
@@ -257,10 +273,12 @@ __device__ __forceinline__ void update_tail(double rz, double rr, double alpha, 
   const double rz_new = reduce_partials(partials, gridDim.x, 2, 0, red);
   const double rr_new = reduce_partials(partials, gridDim.x, 2, 1, red);
   if (threadIdx.x == 0 && sc->nranks > 1) {
-    // distributed: rank partials, reduced by dist_cg_scalar_kernel
+    // distributed: exchange the rank partials and take the scalar step here
+    // (rank-order sums, so every rank gets identical beta / convergence)
     sc->counter[1] = 0;
     sc->rz_loc = rz_new;
     sc->rr_loc = rr_new;
+    if (dd) dist_scalar_step(*dd, sc, rz_new, rr_new, hist, hist_cap, cond, use_cond);
     return;
   }
   if (threadIdx.x == 0) {
@@ -577,6 +595,7 @@ __global__ void __launch_bounds__(K2Layout<n, GROUPS, SPG>::threads, 1)
     cg_update_tma_kernel(const double* __restrict__ w, double* __restrict__ r,
                          const double* __restrict__ dinv, int64_t E, BoxP bx,
                          const int32_t* __restrict__ nbr27, const int64_t* __restrict__ gelem,
+                         const DistDev* __restrict__ dd,
                          CgScalars* __restrict__ sc, double* __restrict__ partials,
                          double* __restrict__ hist, int64_t hist_cap,
                          cudaGraphConditionalHandle cond, int use_cond) {
@@ -770,7 +789,7 @@ __global__ void __launch_bounds__(K2Layout<n, GROUPS, SPG>::threads, 1)
       if (lt == 0) mbar_arrive(&empty[s]);
     }
   }
-  update_tail(rz, rr, alpha, red, &is_last, sc, partials, hist, hist_cap, cond, use_cond);
+  update_tail(rz, rr, alpha, red, &is_last, sc, partials, hist, hist_cap, cond, use_cond, dd);
 }
 
 template <int n>
@@ -944,7 +963,7 @@ cudaError_t launch_k1_tma(const OpDev& op, const double* r, const double* dinv, 
     }
     DParam<n> Dp;
     for (int q = 0; q < n * n; ++q) Dp.d[q] = op.Dh[q];
-    typename Pol::Args a{r, dinv, p, x, w, op.bm, h2, sc, 0.0, 0.0, 0};
+    typename Pol::Args a{r, dinv, p, x, w, op.bm, h2, sc, op.dd, 0.0, 0.0, 0, 0};
     const int64_t NG = (op.E + TmaGeom<n>::EPG - 1) / TmaGeom<n>::EPG;
     int64_t grid = num_sms(dev);
     if (grid > NG) grid = NG;
@@ -960,6 +979,9 @@ cudaError_t launch_k1(const OpDev& op, const double* r, const double* dinv, doub
   using C = AxCfg<n>;
   int dev = 0;
   cudaGetDevice(&dev);
+  // multi-GPU: the halo leaves from the TMA kernel's epilogue, so it is the
+  // only admissible K1 there
+  if (op.dd && !k1_use_tma(op, r, dinv, p, x, h2)) return cudaErrorNotSupported;
   if (k1_use_tma(op, r, dinv, p, x, h2)) {
     if (dinv && h2 != 0.0) return launch_k1_tma<n, true, true>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
     if (dinv) return launch_k1_tma<n, true, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
@@ -1008,7 +1030,7 @@ cudaError_t launch_k2(const OpDev& op, const double* w, double* r, const double*
     if (grid > NG) grid = NG;
     BoxP bx{op.ex, op.ey, op.ez, op.per[0], op.per[1], op.per[2], 0};
     kern<<<(unsigned)grid, L::threads, L::smem, s>>>(w, r, dinv, op.E, bx, op.nbr27, op.gelem,
-                                                     sc, partials, hist, hist_cap, cond,
+                                                     op.dd, sc, partials, hist, hist_cap, cond,
                                                      use_cond);
     return cudaGetLastError();
   }
@@ -1124,13 +1146,13 @@ cudaError_t dist_iteration_tail(const OpDev& op, const DistDev& D, double* w, do
                                 const double* dinv, CgScalars* sc, double* partials,
                                 double* hist, int64_t hist_cap, cudaGraphConditionalHandle cond,
                                 int use_cond, cudaStream_t s) {
-  dist_put_kernel<<<blocks_for(D.send_off[D.nnbr], 256, 296), 256, 0, s>>>(D, 0, 0, w,
-                                                                           &sc->pq_loc, 1);
+  // K1 (already launched) put the halo on the wire from its epilogue and
+  // released phase 0; here: wait + alpha + interface groups, then K2 whose
+  // last CTA exchanges r'z / r'r and takes the scalar step.
   dist_iface_kernel<<<blocks_for(D.n_if, 256, 592), 256, 0, s>>>(D, 0, 0, w, 1, sc);
-  cudaError_t err = k2(op, w, r, dinv, sc, partials, hist, hist_cap, cond, 0, s);
+  cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return err;
-  dist_cg_scalar_kernel<<<1, 32, 0, s>>>(D, sc, hist, hist_cap, cond, use_cond);
-  return cudaGetLastError();
+  return k2(op, w, r, dinv, sc, partials, hist, hist_cap, cond, use_cond, s);
 }
 
 }  // namespace

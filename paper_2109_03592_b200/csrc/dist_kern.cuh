@@ -171,20 +171,16 @@ __global__ void dist_allreduce_kernel(DistDev D, int phase, const double* __rest
   for (int c = 0; c < count; ++c) out[c] = mbox_sum(D, phase, (int)((s + 1) & 1), c);
 }
 
-// End of a distributed CG iteration: all-reduce r'z, r'r (phase 1), then the
-// scalar logic of update_tail (beta, history, convergence, NaN) and the WHILE
-// condition.
-__global__ void dist_cg_scalar_kernel(DistDev D, CgScalars* __restrict__ sc,
-                                      double* __restrict__ hist, int64_t hist_cap,
-                                      cudaGraphConditionalHandle cond, int use_cond) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  if (sc->done) {
-    if (use_cond) cudaGraphSetConditional(cond, 0);
-    return;
-  }
+// End of a distributed CG iteration, run by ONE thread (the last CTA of the
+// update kernel): all-reduce r'z, r'r (phase 1) through the mailboxes, then
+// the scalar logic of update_tail (beta, history, convergence, NaN) and the
+// WHILE condition.
+__device__ void dist_scalar_step(const DistDev& D, CgScalars* __restrict__ sc, double rz_loc,
+                                 double rr_loc, double* __restrict__ hist, int64_t hist_cap,
+                                 cudaGraphConditionalHandle cond, int use_cond) {
   const int phase = 1;
   const unsigned long long s = ld_volatile_u64(D.seq + phase);
-  const double mine[2] = {sc->rz_loc, sc->rr_loc};
+  const double mine[2] = {rz_loc, rr_loc};
   for (int q = 0; q < D.nranks; ++q)
     for (int c = 0; c < 2; ++c)
       D.pmbox[q][mbox_index(phase, (int)((s + 1) & 1), D.rank, c)] = mine[c];
@@ -226,6 +222,42 @@ __global__ void dist_cg_scalar_kernel(DistDev D, CgScalars* __restrict__ sc,
     }
   }
   if (use_cond) cudaGraphSetConditional(cond, sc->done ? 0 : 1);
+}
+
+// Sends of one element-step from the Ax epilogue: the group's threads store
+// the interface values of its element(s) straight into the neighbours'
+// receive buffers (phase 0), then fence at system scope.  Called by every
+// thread of a consumer group; group-uniform control flow.
+__device__ __forceinline__ void dist_send_elements(const DistDev* __restrict__ D, int par,
+                                                   const double* __restrict__ w, int64_t e0,
+                                                   int cnt, int n3, int lt, int tg) {
+  bool stored = false;
+  for (int el = 0; el < cnt; ++el) {
+    const int64_t e = e0 + el;
+    const int lo = D->esend_off[e], hi = D->esend_off[e + 1];
+    for (int c = lo + lt; c < hi; c += tg) {
+      const int qi = D->esend_q[c];
+      const int q = D->nbr[qi];
+      double* dst = D->precv[q] + (int64_t)par * D->precv_total[q] + D->pbase_for_me[q] +
+                    D->esend_pos[c];
+      *dst = w[e * n3 + D->esend_node[c]];
+      stored = true;
+    }
+  }
+  if (stored) __threadfence_system();
+}
+
+// Release of phase 0 by the last CTA of K1 (one thread): this rank's p'Ap
+// partial into every rank's mailbox, then the flags.
+__device__ void dist_release_phase0(const DistDev& D, double pq_loc) {
+  const unsigned long long s = ld_volatile_u64(D.seq);
+  const int par = (int)((s + 1) & 1);
+  __threadfence_system();
+  for (int q = 0; q < D.nranks; ++q) D.pmbox[q][mbox_index(0, par, D.rank, 0)] = pq_loc;
+  __threadfence_system();
+  for (int q = 0; q < D.nranks; ++q)
+    if (q != D.rank) st_release_sys(D.pflags[q] + D.rank, s + 1);
+  D.seq[0] = s + 1;
 }
 
 }  // namespace

@@ -157,6 +157,28 @@ int build_dist_plan(int ex, int ey, int ez, const int* periodic, int degree,
       }
     }
   }
+  {
+    // regroup the send lists by local element
+    const size_t EL = P.loc_elems.size();
+    std::vector<int32_t> cnt(EL + 1, 0);
+    for (size_t qi = 0; qi < NQ; ++qi)
+      for (int32_t a : P.send_idx[qi]) ++cnt[a / n3 + 1];
+    for (size_t e = 0; e < EL; ++e) cnt[e + 1] += cnt[e];
+    P.esend_off = cnt;
+    const size_t tot = (size_t)cnt[EL];
+    P.esend_node.assign(tot, 0);
+    P.esend_q.assign(tot, 0);
+    P.esend_pos.assign(tot, 0);
+    std::vector<int32_t> fill(cnt.begin(), cnt.end() - 1);
+    for (size_t qi = 0; qi < NQ; ++qi)
+      for (size_t i = 0; i < P.send_idx[qi].size(); ++i) {
+        const int32_t a = P.send_idx[qi][i];
+        const int32_t slot = fill[a / n3]++;
+        P.esend_node[slot] = (int32_t)(a % n3);
+        P.esend_q[slot] = (int32_t)qi;
+        P.esend_pos[slot] = (int32_t)i;
+      }
+  }
   P.recv_base.assign(NQ, 0);
   for (size_t qi = 1; qi < NQ; ++qi) P.recv_base[qi] = P.recv_base[qi - 1] + P.recv_count[qi - 1];
   P.recv_total = NQ ? P.recv_base[NQ - 1] + P.recv_count[NQ - 1] : 0;

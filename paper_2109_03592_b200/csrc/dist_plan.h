@@ -36,6 +36,10 @@ struct DistPlan {
   std::vector<std::vector<int32_t>> send_idx;
   std::vector<int64_t> recv_count, recv_base;  // recv_base: offset of nbr q's block
   int64_t recv_total = 0;
+  // the same sends regrouped by local element (for sending from the Ax
+  // epilogue): per entry the node within the element, the neighbour index and
+  // the position inside that neighbour's block
+  std::vector<int32_t> esend_off, esend_node, esend_q, esend_pos;
   // 27-neighbourhood of every local element: local id, -1 outside the
   // domain, -2 on another rank ((dx+1) + 3(dy+1) + 9(dz+1))
   std::vector<int32_t> nbr27;

@@ -7,6 +7,8 @@
 
 namespace sbx {
 
+struct DistDev;
+
 // Operator data resident in HBM.
 struct OpDev {
   int64_t E = 0;
@@ -38,6 +40,7 @@ struct OpDev {
   bool table = false;
   const int32_t* nbr27 = nullptr;
   const int64_t* gelem = nullptr;
+  const DistDev* dd = nullptr;  // device copy of the exchange state (multi-GPU)
 };
 
 // Device-resident CG scalars for the fused (FAST) solver.
@@ -100,6 +103,11 @@ struct DistDev {
   const int32_t* if_code = nullptr;
   const int32_t* nbr27 = nullptr;  // local elements' 27-neighbourhood
   const int64_t* gelem = nullptr;  // global element id of each local element
+  // sends regrouped by local element (K1 epilogue puts them on the wire)
+  const int32_t* esend_off = nullptr;
+  const int32_t* esend_node = nullptr;
+  const int32_t* esend_q = nullptr;
+  const int32_t* esend_pos = nullptr;
   unsigned long long* seq = nullptr;  // device [4]
   unsigned int* counter = nullptr;    // device [4]
   int* status = nullptr;              // device: 1 on exchange timeout
