@@ -922,8 +922,8 @@ namespace {
 
 struct DistBlob {
   cudaIpcMemHandle_t handle;
-  int64_t recv_total;
-  int64_t recv_base_for_src[kMaxRanks];
+  int64_t send_total;                 // size of one send-buffer parity region
+  int64_t send_base_for_dst[kMaxRanks];  // my block destined to rank q (-1: none)
 };
 
 sbx_status upload_dist(sbx_ctx* c, const DistPlan& P, const sbx_box_desc* d) {
@@ -1028,6 +1028,9 @@ sbx_status upload_dist(sbx_ctx* c, const DistPlan& P, const sbx_box_desc* d) {
   D.nbr27 = n27;
   D.gelem = ge;
   D.recv_total = P.recv_total;
+  D.send_total = D.send_off[D.nnbr];
+  for (int qi = 0; qi < D.nnbr; ++qi) D.recv_base[qi] = P.recv_base[qi];
+  D.recv_base[D.nnbr] = P.recv_total;
   void* p = nullptr;
   SBX_TRY(dalloc(c, &p, 4 * sizeof(unsigned long long)));
   D.seq = static_cast<unsigned long long*>(p);
@@ -1040,15 +1043,17 @@ sbx_status upload_dist(sbx_ctx* c, const DistPlan& P, const sbx_box_desc* d) {
   SBX_CUDA(cudaMemsetAsync(D.status, 0, sizeof(int), c->stream));
   // peer window (exported over CUDA IPC; own allocation, not via dalloc's list
   // so it is freed after the peers close their mappings)
-  const size_t wbytes = kWinRecv + sizeof(double) * (size_t)std::max<int64_t>(4 * P.recv_total, 2);
+  const size_t wbytes =
+      kWinRecv + sizeof(double) * (size_t)std::max<int64_t>(4 * D.send_total, 2);
   SBX_CUDA(cudaMalloc(&c->window, wbytes));
   SBX_CUDA(cudaMemsetAsync(c->window, 0, wbytes, c->stream));
   char* wb = static_cast<char*>(c->window);
   D.flags = reinterpret_cast<unsigned long long*>(wb + kWinFlags);
   D.mbox = reinterpret_cast<double*>(wb + kWinMbox);
-  D.recv = reinterpret_cast<double*>(wb + kWinRecv);
+  D.sendb = reinterpret_cast<double*>(wb + kWinRecv);
+  // per destination rank: offset of its block in my send buffer (-1: none)
   c->recv_base_for_src.assign(kMaxRanks, -1);
-  for (int qi = 0; qi < D.nnbr; ++qi) c->recv_base_for_src[P.nbr[qi]] = P.recv_base[qi];
+  for (int qi = 0; qi < D.nnbr; ++qi) c->recv_base_for_src[P.nbr[qi]] = D.send_off[qi];
   SBX_TRY(ensure_partials(c, std::max<int64_t>(EL, 4096)));
   c->cg.reset(new CgEngine());
   SBX_CUDA(cudaStreamSynchronize(c->stream));
@@ -1114,8 +1119,8 @@ sbx_status sbx_ctx_dist_blob(sbx_ctx* c, uint8_t* blob) {
   DistBlob b;
   std::memset(&b, 0, sizeof(b));
   SBX_CUDA(cudaIpcGetMemHandle(&b.handle, c->window));
-  b.recv_total = c->dd.recv_total;
-  for (int q = 0; q < kMaxRanks; ++q) b.recv_base_for_src[q] = c->recv_base_for_src[q];
+  b.send_total = c->dd.send_total;
+  for (int q = 0; q < kMaxRanks; ++q) b.send_base_for_dst[q] = c->recv_base_for_src[q];
   std::memcpy(blob, &b, sizeof(b));
   return SBX_OK;
 }
@@ -1142,15 +1147,15 @@ sbx_status sbx_ctx_dist_connect(sbx_ctx* c, const uint8_t* blobs) {
     }
     D.pflags[q] = reinterpret_cast<unsigned long long*>(base + kWinFlags);
     D.pmbox[q] = reinterpret_cast<double*>(base + kWinMbox);
-    D.precv[q] = reinterpret_cast<double*>(base + kWinRecv);
-    D.precv_total[q] = b.recv_total;
-    D.pbase_for_me[q] = b.recv_base_for_src[c->rank];
+    D.psend[q] = reinterpret_cast<double*>(base + kWinRecv);
+    D.psend_total[q] = b.send_total;
+    D.pbase_from[q] = b.send_base_for_dst[c->rank];
     if (q != c->rank) {
-      // a neighbour must have a receive block for me, and I for it
+      // a neighbour must hold a send block for me, and I for it
       bool i_send = false;
       for (int qi = 0; qi < D.nnbr; ++qi)
         if (D.nbr[qi] == q) i_send = true;
-      if (i_send != (b.recv_base_for_src[c->rank] >= 0)) {
+      if (i_send != (b.send_base_for_dst[c->rank] >= 0)) {
         set_error("sbx_ctx_dist_connect: inconsistent exchange plans between ranks");
         return SBX_E_COMM;
       }
@@ -1158,6 +1163,7 @@ sbx_status sbx_ctx_dist_connect(sbx_ctx* c, const uint8_t* blobs) {
   }
   // device copy of the exchange state for the fused kernels (K1 epilogue
   // sends, K2 scalar step)
+  D.debug_nosend = std::getenv("SBX_DEBUG_NOSEND") ? 1 : 0;
   void* p = nullptr;
   SBX_TRY(dalloc(c, &p, sizeof(DistDev)));
   SBX_CUDA(cudaMemcpy(p, &c->dd, sizeof(DistDev), cudaMemcpyHostToDevice));

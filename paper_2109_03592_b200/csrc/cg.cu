@@ -96,7 +96,8 @@ struct CgK1Pol {
     const DistDev* dd;  // multi-GPU: interface values go out from the epilogue
     double beta, ap;
     int first;
-    int par;  // receive-buffer parity of this iteration's halo (phase 0)
+    int par;  // send-buffer parity of this iteration's halo (phase 0)
+    const int32_t* esend_off;
   };
   __device__ static bool init(Args& a) {
     if (a.sc->done) return false;
@@ -104,14 +105,21 @@ struct CgK1Pol {
     a.beta = a.sc->beta;
     a.ap = a.sc->alpha_prev;
     a.par = a.dd ? (int)((*(const volatile unsigned long long*)a.dd->seq + 1) & 1) : 0;
+    a.esend_off = a.dd ? a.dd->esend_off : nullptr;
+    if (a.dd && a.dd->debug_nosend) a.esend_off = nullptr;  // timing experiments only
     return true;
   }
-  // after the element(s) of a step are written: put their interface values on
-  // the wire (group-uniform; no-op on a single GPU)
-  __device__ static void element_done(const Args& a, int64_t e0, int cnt, int n3, int lt,
-                                      int tg, int bar) {
-    if (!a.dd) return;
-    if (a.dd->esend_off[e0] == a.dd->esend_off[e0 + cnt]) return;
+  // number of interface sends of a step's element(s): read by the producer
+  // lane one step ahead and handed to the consumers through the slot metadata
+  __device__ static int element_sends(const Args& a, int64_t e0, int cnt) {
+    if (!a.esend_off) return 0;
+    return __ldg(a.esend_off + e0 + cnt) - __ldg(a.esend_off + e0);
+  }
+  // after the element(s) of a step are written: put their interface values in
+  // the send buffer (group-uniform; no-op on a single GPU)
+  __device__ static void element_done(const Args& a, int nsend, int64_t e0, int cnt, int n3,
+                                      int lt, int tg, int bar) {
+    if (nsend == 0) return;
     named_bar_sync(bar, tg);  // w of the step visible to the whole group
     dist_send_elements(a.dd, a.par, a.w, e0, cnt, n3, lt, tg);
   }
@@ -143,17 +151,20 @@ struct CgK1Pol {
 template <bool HAS_DINV, bool HAS_BM>
 __device__ void CgK1Pol<HAS_DINV, HAS_BM>::finish(const Args& a, double red, double* partials,
                                                   double* sh, bool* flag) {
+  // (dist: the CTA's send-buffer stores are published by last_block's
+  // barrier + GPU-scope fence before the ticket, then released at system
+  // scope by dist_release_phase0)
   const double v = cta_sum(red, sh);
   if (threadIdx.x == 0) partials[blockIdx.x] = v;
   CgScalars* sc = a.sc;
   if (!last_block(&sc->counter[0], flag)) return;
   const double tot = reduce_partials(partials, gridDim.x, 1, 0, sh);
-  if (threadIdx.x == 0 && sc->nranks > 1) {
+  if (threadIdx.x == 0 && a.dd) {
     sc->counter[0] = 0;
     sc->pq_loc = tot;  // summed over ranks by dist_iface_kernel
     // every CTA fenced its interface stores before its ticket: release the
     // halo and this rank's p'Ap to all ranks
-    if (a.dd) dist_release_phase0(*a.dd, tot);
+    dist_release_phase0(*a.dd, tot);
     return;
   }
   if (threadIdx.x == 0) {
@@ -272,13 +283,13 @@ __device__ __forceinline__ void update_tail(double rz, double rr, double alpha, 
   if (!last_block(&sc->counter[1], is_last)) return;
   const double rz_new = reduce_partials(partials, gridDim.x, 2, 0, red);
   const double rr_new = reduce_partials(partials, gridDim.x, 2, 1, red);
-  if (threadIdx.x == 0 && sc->nranks > 1) {
+  if (threadIdx.x == 0 && dd) {
     // distributed: exchange the rank partials and take the scalar step here
     // (rank-order sums, so every rank gets identical beta / convergence)
     sc->counter[1] = 0;
     sc->rz_loc = rz_new;
     sc->rr_loc = rr_new;
-    if (dd) dist_scalar_step(*dd, sc, rz_new, rr_new, hist, hist_cap, cond, use_cond);
+    dist_scalar_step(*dd, sc, rz_new, rr_new, hist, hist_cap, cond, use_cond);
     return;
   }
   if (threadIdx.x == 0) {
@@ -558,7 +569,10 @@ __global__ void __launch_bounds__(AxCfg<n>::threads)
 // columns are streamed into shared memory by a producer warp with 1-D TMA
 // bulk copies (ring of slots owned per consumer group, as in ax_tma_kernel),
 // so HBM latency is hidden by the ring and registers stay free for the
-// partner-copy gathers, which hit L2.
+// partner-copy gathers, which hit L2.  The producer warp also writes, per
+// element of a slot, its 27-neighbourhood (lane l: neighbour (l%3-1,
+// l/3%3-1, l/9-1) as a local element id, -1 outside the domain = Dirichlet
+// face, -2 on another rank), so the consumers do no index arithmetic.
 template <int n, int GROUPS, int SPG>
 struct K2Layout {
   using T = TmaGeom<n>;
@@ -566,14 +580,16 @@ struct K2Layout {
   static constexpr int SLOT_D = 3 * V_D;
   static constexpr int S = GROUPS * SPG;
   static constexpr size_t BAR_BYTES = ((2 * S * 8 + 127) / 128) * 128;  // full[S] + empty[S]
-  static constexpr size_t smem = BAR_BYTES + sizeof(double) * (size_t)S * SLOT_D;
+  static constexpr size_t META_BYTES = (size_t)S * T::EPG * 32 * 4;
+  static constexpr size_t smem = BAR_BYTES + META_BYTES + sizeof(double) * (size_t)S * SLOT_D;
   static constexpr int threads = GROUPS * T::TG + 32;
 };
 
 template <int n>
 struct K2Choice {
   using T = TmaGeom<n>;
-  static constexpr size_t slot_bytes = sizeof(double) * K2Layout<n, 1, 1>::SLOT_D;
+  static constexpr size_t slot_bytes =
+      sizeof(double) * K2Layout<n, 1, 1>::SLOT_D + (size_t)T::EPG * 32 * 4;
   static constexpr int pick() {
     for (int g = 16; g >= 1; --g) {
       if (g * T::TG + 32 > 1024) continue;
@@ -590,12 +606,15 @@ struct K2Choice {
   static constexpr int SPG = spg();
 };
 
+// neighbour code: >= 0 local element, -1 outside (Dirichlet), -2 other rank,
+// -3 the node is not on that face (no partner)
+__device__ __forceinline__ bool nb_act(int c) { return c >= 0 || c == -2; }
+
 template <int n, int GROUPS, int SPG, bool TABLE>
 __global__ void __launch_bounds__(K2Layout<n, GROUPS, SPG>::threads, 1)
     cg_update_tma_kernel(const double* __restrict__ w, double* __restrict__ r,
                          const double* __restrict__ dinv, int64_t E, BoxP bx,
-                         const int32_t* __restrict__ nbr27, const int64_t* __restrict__ gelem,
-                         const DistDev* __restrict__ dd,
+                         const int32_t* __restrict__ nbr27, const DistDev* __restrict__ dd,
                          CgScalars* __restrict__ sc, double* __restrict__ partials,
                          double* __restrict__ hist, int64_t hist_cap,
                          cudaGraphConditionalHandle cond, int use_cond) {
@@ -603,6 +622,7 @@ __global__ void __launch_bounds__(K2Layout<n, GROUPS, SPG>::threads, 1)
   using L = K2Layout<n, GROUPS, SPG>;
   constexpr int S = L::S;
   constexpr int N = n - 1;
+  constexpr int EPG = T::EPG;
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ double red[32];
   __shared__ bool is_last;
@@ -613,12 +633,13 @@ __global__ void __launch_bounds__(K2Layout<n, GROUPS, SPG>::threads, 1)
   const double alpha = sc->alpha;
   uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
   uint64_t* empty = full + S;
-  double* slots = reinterpret_cast<double*>(smraw + L::BAR_BYTES);
-  const int64_t NG = (E + T::EPG - 1) / T::EPG;
+  int32_t* meta = reinterpret_cast<int32_t*>(smraw + L::BAR_BYTES);  // [S][EPG][32]
+  double* slots = reinterpret_cast<double*>(smraw + L::BAR_BYTES + L::META_BYTES);
+  const int64_t NG = (E + EPG - 1) / EPG;
   const int64_t M = NG > (int64_t)blockIdx.x ? (NG - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], 32);  // every producer lane arrives (meta), lane 0 with the bytes
       mbar_init(&empty[s], 1);
     }
     mbar_fence_init();
@@ -627,12 +648,44 @@ __global__ void __launch_bounds__(K2Layout<n, GROUPS, SPG>::threads, 1)
   double rz = 0.0, rr = 0.0;
   const int warp = threadIdx.x >> 5;
   if (warp == GROUPS * T::TG / 32) {
-    if ((threadIdx.x & 31) == 0) {
-      for (int64_t m = 0; m < M; ++m) {
-        const int s = (int)(m % S);
-        if (m >= S) mbar_wait(&empty[s], (uint32_t)((m / S - 1) & 1));
-        const int64_t e0 = (blockIdx.x + m * gridDim.x) * T::EPG;
-        const int64_t cnt = (E - e0) < T::EPG ? (E - e0) : T::EPG;
+    // ---------------- producer warp --------------------------------------
+    const int lane = threadIdx.x & 31;
+    const int dx = lane % 3 - 1, dy = (lane / 3) % 3 - 1, dz = lane / 9 - 1;
+    // neighbour `lane` of element e (box lattice, or this rank's table)
+    auto nb_of = [&](int64_t e) -> int32_t {
+      if (lane >= 27 || e >= E) return -1;
+      if constexpr (TABLE) {
+        return __ldg(nbr27 + e * 27 + lane);
+      } else {
+        const uint32_t ue = (uint32_t)e, uex = (uint32_t)bx.ex, uey = (uint32_t)bx.ey;
+        const uint32_t q = ue / uex;
+        int x = (int)(ue - q * uex) + dx, y = (int)(q % uey) + dy, z = (int)(q / uey) + dz;
+        if (x < 0 || x >= bx.ex) {
+          if (!bx.px) return -1;
+          x = x < 0 ? bx.ex - 1 : 0;
+        }
+        if (y < 0 || y >= bx.ey) {
+          if (!bx.py) return -1;
+          y = y < 0 ? bx.ey - 1 : 0;
+        }
+        if (z < 0 || z >= bx.ez) {
+          if (!bx.pz) return -1;
+          z = z < 0 ? bx.ez - 1 : 0;
+        }
+        return (int32_t)(x + bx.ex * (y + bx.ey * z));
+      }
+    };
+    int32_t nxt[EPG];  // loaded one step ahead (table mode: hides the load)
+    if (M > 0) {
+#pragma unroll
+      for (int el = 0; el < EPG; ++el) nxt[el] = nb_of((int64_t)blockIdx.x * EPG + el);
+    }
+    for (int64_t m = 0; m < M; ++m) {
+      const int s = (int)(m % S);
+      if (m >= S) mbar_wait(&empty[s], (uint32_t)((m / S - 1) & 1));
+      const int64_t e0 = (blockIdx.x + m * gridDim.x) * EPG;
+      if (lane == 0) {
+        const int64_t cnt = (E - e0) < EPG ? (E - e0) : EPG;
         const int shift = (int)((e0 * T::n3) & 1);
         const uint32_t vb = (uint32_t)((((cnt * T::n3 + shift) * 8) + 15) / 16 * 16);
         double* slot = slots + s * L::SLOT_D;
@@ -641,143 +694,92 @@ __global__ void __launch_bounds__(K2Layout<n, GROUPS, SPG>::threads, 1)
         tma_load_1d(slot + L::V_D, r + e0 * T::n3 - shift, vb, &full[s]);
         if (dinv) tma_load_1d(slot + 2 * L::V_D, dinv + e0 * T::n3 - shift, vb, &full[s]);
       }
+#pragma unroll
+      for (int el = 0; el < EPG; ++el) meta[(s * EPG + el) * 32 + lane] = nxt[el];
+      if (lane != 0) mbar_arrive(&full[s]);
+      if (m + 1 < M) {
+        const int64_t e1 = (blockIdx.x + (m + 1) * gridDim.x) * EPG;
+#pragma unroll
+        for (int el = 0; el < EPG; ++el) nxt[el] = nb_of(e1 + el);
+      }
     }
   } else {
+    // ---------------- consumer groups ------------------------------------
     const int g = threadIdx.x / T::TG, lt = threadIdx.x % T::TG;
     const int sl = lt / T::nn, ij = lt % T::nn, i = ij % n, j = ij / n;
-    const bool act = sl < T::EPG;
-    const int64_t exy = (int64_t)bx.ex * bx.ey;
+    const bool act = sl < EPG;
+    // thread constants: which x / y face the column (i, j) lies on
+    const int xi = i == 0 ? 0 : (i == N ? 2 : 1), yi = j == 0 ? 0 : (j == N ? 2 : 1);
+    const bool xs = xi != 1, ys = yi != 1;
+    const int cxo = j * n + (N - i), cyo = (N - j) * n + i, cxyo = (N - j) * n + (N - i);
     for (int64_t m = g; m < M; m += GROUPS) {
       const int s = (int)(m % S);
-      const int64_t e = (blockIdx.x + m * gridDim.x) * T::EPG + sl;
+      const int64_t e = (blockIdx.x + m * gridDim.x) * EPG + sl;
       const bool valid = act && e < E;
-      // partner-copy addresses do not depend on the slot: issue the gathers
-      // before waiting for the TMA bytes
-      Dir X{0, false, false, 0}, Y = X, Z0 = X, ZN = X;
-      const double *pw = w, *px = w, *py = w, *pxy = w;
-      // columns (own, x, y, xy) of the element across the k=0 / k=N faces
-      const double *z0p0 = w, *z0p1 = w, *z0p2 = w, *z0p3 = w;
-      const double *zNp0 = w, *zNp1 = w, *zNp2 = w, *zNp3 = w;
-      // TABLE (multi-GPU): a partner on another rank marks an interface group,
-      // already assembled in w by dist_iface_kernel
-      bool rem_xy = false, rem_z0 = false, rem_zN = false;
-      if (valid) {
-        const int64_t ge = TABLE ? gelem[e] : e;
-        const int cx = (int)(ge % bx.ex), cy = (int)((ge / bx.ex) % bx.ey);
-        const int cz = (int)(ge / exy);
-        X = dir_state(i, N, cx, bx.ex, bx.px, 1);
-        Y = dir_state(j, N, cy, bx.ey, bx.py, bx.ex);
-        Z0 = dir_state(0, N, cz, bx.ez, bx.pz, exy);
-        ZN = dir_state(N, N, cz, bx.ez, bx.pz, exy);
-        const int64_t cxo = j * n + (N - i), cyo = (N - j) * n + i, cxyo = (N - j) * n + (N - i);
-        if constexpr (TABLE) {
-          const int32_t* t = nbr27 + e * 27;
-          const int dxi = i == 0 ? 0 : 2, dyi = j == 0 ? 0 : 2;
-          auto id = [&](int xi, int yi, int zi) { return t[xi + 3 * yi + 9 * zi]; };
-          const int32_t lx = X.act ? id(dxi, 1, 1) : 0, ly = Y.act ? id(1, dyi, 1) : 0;
-          const int32_t lxy = (X.act && Y.act) ? id(dxi, dyi, 1) : 0;
-          rem_xy = lx < 0 || ly < 0 || lxy < 0;
-          pw = w + e * T::n3 + ij;
-          px = w + (int64_t)(lx < 0 ? 0 : lx) * T::n3 + cxo;
-          py = w + (int64_t)(ly < 0 ? 0 : ly) * T::n3 + cyo;
-          pxy = w + (int64_t)(lxy < 0 ? 0 : lxy) * T::n3 + cxyo;
-          const int zf[2] = {0, 2};
-          for (int f = 0; f < 2; ++f) {
-            const Dir& Z = f == 0 ? Z0 : ZN;
-            if (!Z.act) continue;
-            const int32_t l0 = id(1, 1, zf[f]);
-            const int32_t l1 = X.act ? id(dxi, 1, zf[f]) : 0;
-            const int32_t l2 = Y.act ? id(1, dyi, zf[f]) : 0;
-            const int32_t l3 = (X.act && Y.act) ? id(dxi, dyi, zf[f]) : 0;
-            const bool rem = rem_xy || l0 < 0 || l1 < 0 || l2 < 0 || l3 < 0;
-            const int64_t ko = (f == 0 ? N : 0) * T::nn;
-            const double* c0 = w + (int64_t)(l0 < 0 ? 0 : l0) * T::n3 + ij + ko;
-            const double* c1 = w + (int64_t)(l1 < 0 ? 0 : l1) * T::n3 + cxo + ko;
-            const double* c2 = w + (int64_t)(l2 < 0 ? 0 : l2) * T::n3 + cyo + ko;
-            const double* c3 = w + (int64_t)(l3 < 0 ? 0 : l3) * T::n3 + cxyo + ko;
-            if (f == 0) {
-              z0p0 = c0, z0p1 = c1, z0p2 = c2, z0p3 = c3, rem_z0 = rem;
-            } else {
-              zNp0 = c0, zNp1 = c1, zNp2 = c2, zNp3 = c3, rem_zN = rem;
-            }
-          }
-        } else {
-          pw = w + e * T::n3 + ij;
-          px = w + (e + X.d) * T::n3 + cxo;
-          py = w + (e + Y.d) * T::n3 + cyo;
-          pxy = w + (e + X.d + Y.d) * T::n3 + cxyo;
-          const int64_t o0 = Z0.d * T::n3 + N * T::nn, oN = ZN.d * T::n3;
-          z0p0 = pw + o0, z0p1 = px + o0, z0p2 = py + o0, z0p3 = pxy + o0;
-          zNp0 = pw + oN, zNp1 = px + oN, zNp2 = py + oN, zNp3 = pxy + oN;
-        }
-      }
-      const bool axy = X.act && Y.act;
-      double wx[n], wy[n], wxy[n];
-#pragma unroll
-      for (int k = 0; k < n; ++k) {
-        const bool rk = k == 0 ? rem_z0 : (k == N ? rem_zN : rem_xy);
-        wx[k] = (X.act && !rk) ? __ldg(px + k * T::nn) : 0.0;
-        wy[k] = (Y.act && !rk) ? __ldg(py + k * T::nn) : 0.0;
-        wxy[k] = (axy && !rk) ? __ldg(pxy + k * T::nn) : 0.0;
-      }
-      double z0c0 = 0, z0c1 = 0, z0c2 = 0, z0c3 = 0, zNc0 = 0, zNc1 = 0, zNc2 = 0, zNc3 = 0;
-      if (Z0.act && !rem_z0) {
-        z0c0 = __ldg(z0p0);
-        if (X.act) z0c1 = __ldg(z0p1);
-        if (Y.act) z0c2 = __ldg(z0p2);
-        if (axy) z0c3 = __ldg(z0p3);
-      }
-      if (ZN.act && !rem_zN) {
-        zNc0 = __ldg(zNp0);
-        if (X.act) zNc1 = __ldg(zNp1);
-        if (Y.act) zNc2 = __ldg(zNp2);
-        if (axy) zNc3 = __ldg(zNp3);
-      }
       mbar_wait(&full[s], (uint32_t)((m / S) & 1));
-      const int shift = (int)(((e - sl) * T::n3) & 1);
-      const double* slot = slots + s * L::SLOT_D + shift + sl * T::n3 + ij;
       if (valid) {
-        const bool mxy = X.msk || Y.msk;
-        const int cxy = X.act + Y.act;
+        const int32_t* nb = meta + (s * EPG + sl) * 32;
+        auto at = [&](int a, int b, int c) { return nb[a + 3 * b + 9 * c]; };
+        const int lx = xs ? at(xi, 1, 1) : -3, ly = ys ? at(1, yi, 1) : -3;
+        const int lxy = (xs && ys) ? at(xi, yi, 1) : -3;
+        const int z0 = at(1, 1, 0), zN = at(1, 1, 2);
+        const int z0x = xs ? at(xi, 1, 0) : -3, zNx = xs ? at(xi, 1, 2) : -3;
+        const int z0y = ys ? at(1, yi, 0) : -3, zNy = ys ? at(1, yi, 2) : -3;
+        const int z0xy = (xs && ys) ? at(xi, yi, 0) : -3, zNxy = (xs && ys) ? at(xi, yi, 2) : -3;
+        const bool ax = nb_act(lx), ay = nb_act(ly), az0 = nb_act(z0), azN = nb_act(zN);
+        const bool mxy = lx == -1 || ly == -1;
+        const bool m0 = z0 == -1, mN = zN == -1;
+        // interface nodes (a copy on another rank) were assembled by
+        // dist_iface_kernel: own value only
+        bool rem_xy = false, rem_z0 = false, rem_zN = false;
+        if constexpr (TABLE) {
+          rem_xy = lx == -2 || ly == -2 || lxy == -2;
+          rem_z0 = rem_xy || z0 == -2 || z0x == -2 || z0y == -2 || z0xy == -2;
+          rem_zN = rem_xy || zN == -2 || zNx == -2 || zNy == -2 || zNxy == -2;
+        }
+        // partner-copy gathers (L2): x, y, xy columns and the z-face rows
+        double wx[n], wy[n], wxy[n];
+        const double* px = w + (int64_t)(lx < 0 ? 0 : lx) * T::n3 + cxo;
+        const double* py = w + (int64_t)(ly < 0 ? 0 : ly) * T::n3 + cyo;
+        const double* pxy = w + (int64_t)(lxy < 0 ? 0 : lxy) * T::n3 + cxyo;
+#pragma unroll
+        for (int k = 0; k < n; ++k) {
+          const bool rk = k == 0 ? rem_z0 : (k == N ? rem_zN : rem_xy);
+          wx[k] = (lx >= 0 && !rk) ? __ldg(px + k * T::nn) : 0.0;
+          wy[k] = (ly >= 0 && !rk) ? __ldg(py + k * T::nn) : 0.0;
+          wxy[k] = (lxy >= 0 && !rk) ? __ldg(pxy + k * T::nn) : 0.0;
+        }
+        auto zld = [&](int l, int off, bool rk) {
+          return (l >= 0 && !rk) ? __ldg(w + (int64_t)l * T::n3 + off) : 0.0;
+        };
+        // plane N of the element below / plane 0 of the element above
+        const double a0 = zld(z0, N * T::nn + ij, rem_z0), a1 = zld(z0x, N * T::nn + cxo, rem_z0);
+        const double a2 = zld(z0y, N * T::nn + cyo, rem_z0);
+        const double a3 = zld(z0xy, N * T::nn + cxyo, rem_z0);
+        const double b0 = zld(zN, ij, rem_zN), b1 = zld(zNx, cxo, rem_zN);
+        const double b2 = zld(zNy, cyo, rem_zN), b3 = zld(zNxy, cxyo, rem_zN);
+        const double zs0 = (a0 + a1) + (a2 + a3), zsN = (b0 + b1) + (b2 + b3);
+        const double wgt_xy = (ax ? 0.5 : 1.0) * (ay ? 0.5 : 1.0);
+        const int shift = (int)(((e - sl) * T::n3) & 1);
+        const double* slot = slots + s * L::SLOT_D + shift + sl * T::n3 + ij;
         double* rp = r + e * T::n3 + ij;
 #pragma unroll
         for (int k = 0; k < n; ++k) {
           const double wo = slot[k * T::nn];
           const double ro = slot[L::V_D + k * T::nn];
           const double dv = dinv ? slot[2 * L::V_D + k * T::nn] : 1.0;
-          const Dir Z = k == 0 ? Z0 : (k == N ? ZN : Dir{0, false, false, 0});
-          double q;
-          const bool rk = k == 0 ? rem_z0 : (k == N ? rem_zN : rem_xy);
-          const bool msk = mxy || ((k == 0 || k == N) && Z.msk);
-          // Branch-free canonical sum over the 8 copy slots (z-side outer, y,
-          // x inner; in each direction the smaller cell first).  Inactive
-          // slots add +0.0; every copy of a node runs the identical sequence,
-          // so all copies get the same bits.  Interface nodes (rk) were
-          // assembled by dist_iface_kernel: own value only.
-          const bool ax = X.act && !rk, ay = Y.act && !rk, az = Z.act && !rk;
-          const bool lo = (k == 0);
-          const double zc0 = lo ? z0c0 : zNc0, zc1 = lo ? z0c1 : zNc1;
-          const double zc2 = lo ? z0c2 : zNc2, zc3 = lo ? z0c3 : zNc3;
-          double sum = 0.0;
-#pragma unroll
-          for (int zs = 0; zs < 2; ++zs) {
-#pragma unroll
-            for (int ys = 0; ys < 2; ++ys) {
-#pragma unroll
-              for (int xs = 0; xs < 2; ++xs) {
-                const bool on = (zs == 0 || az) && (ys == 0 || ay) && (xs == 0 || ax);
-                const bool zn = az && ((zs == 0) == Z.nfirst);
-                const bool yn = ay && ((ys == 0) == Y.nfirst);
-                const bool xn = ax && ((xs == 0) == X.nfirst);
-                const double vp = yn ? (xn ? wxy[k] : wy[k]) : (xn ? wx[k] : wo);
-                const double vz = yn ? (xn ? zc3 : zc2) : (xn ? zc1 : zc0);
-                sum += on ? (zn ? vz : vp) : 0.0;
-              }
-            }
-          }
-          q = msk ? 0.0 : sum;
-          const int cnt = cxy + Z.act;
-          const double wgt = cnt == 0 ? 1.0 : cnt == 1 ? 0.5 : cnt == 2 ? 0.25 : 0.125;
+          // Pairwise tree over the copies: x-pairs, the y-pair of x-pairs,
+          // then the z-pair of planes.  Each level adds exactly two operands
+          // (an absent partner contributes +0.0 in the same position for
+          // every copy) and IEEE addition is commutative, so every copy of a
+          // node gets the same bits with no ordering logic.
+          double sum = (wo + wx[k]) + (wy[k] + wxy[k]);
+          if (k == 0) sum = sum + zs0;
+          if (k == N) sum = sum + zsN;
+          const bool msk = mxy || (k == 0 && m0) || (k == N && mN);
+          const double q = msk ? 0.0 : sum;
+          const double wgt =
+              k == 0 ? (az0 ? 0.5 * wgt_xy : wgt_xy) : (k == N ? (azN ? 0.5 * wgt_xy : wgt_xy) : wgt_xy);
           const double rv = fma(-alpha, q, ro);
           rp[k * T::nn] = rv;
           const double z = rv * dv;
@@ -963,7 +965,7 @@ cudaError_t launch_k1_tma(const OpDev& op, const double* r, const double* dinv, 
     }
     DParam<n> Dp;
     for (int q = 0; q < n * n; ++q) Dp.d[q] = op.Dh[q];
-    typename Pol::Args a{r, dinv, p, x, w, op.bm, h2, sc, op.dd, 0.0, 0.0, 0, 0};
+    typename Pol::Args a{r, dinv, p, x, w, op.bm, h2, sc, op.dd, 0.0, 0.0, 0, 0, nullptr};
     const int64_t NG = (op.E + TmaGeom<n>::EPG - 1) / TmaGeom<n>::EPG;
     int64_t grid = num_sms(dev);
     if (grid > NG) grid = NG;
@@ -1029,9 +1031,8 @@ cudaError_t launch_k2(const OpDev& op, const double* w, double* r, const double*
     int64_t grid = num_sms(dev);
     if (grid > NG) grid = NG;
     BoxP bx{op.ex, op.ey, op.ez, op.per[0], op.per[1], op.per[2], 0};
-    kern<<<(unsigned)grid, L::threads, L::smem, s>>>(w, r, dinv, op.E, bx, op.nbr27, op.gelem,
-                                                     op.dd, sc, partials, hist, hist_cap, cond,
-                                                     use_cond);
+    kern<<<(unsigned)grid, L::threads, L::smem, s>>>(w, r, dinv, op.E, bx, op.nbr27, op.dd, sc,
+                                                     partials, hist, hist_cap, cond, use_cond);
     return cudaGetLastError();
   }
   if (op.box && use_flat) {

@@ -1,9 +1,9 @@
 // Peer-window exchange kernels for the distributed PCG (included by cg.cu).
 //
-// A sender stores raw copy values straight into the receiver's window over
-// NVLink (plain st.global on IPC-mapped peer pointers), fences at system
-// scope, and releases a per-(phase, source) sequence flag; the receiver
-// acquires the flags of all ranks, then reads its window.  Scalars travel in
+// A sender writes raw copy values into its OWN send buffer, publishes them at
+// GPU scope and releases a per-(phase, source) sequence flag in every peer's
+// window; the receiver acquires the flags of all ranks, then pulls the blocks
+// destined to it over NVLink (IPC-mapped peer pointers).  Scalars travel in
 // per-source mailboxes and are summed in rank order, so every rank computes
 // bit-identical CG scalars.  Waits are bounded (kSpinTimeoutNs) and report a
 // communication error instead of hanging.
@@ -36,6 +36,14 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
+// Publication rule: values are made visible at GPU scope (__threadfence; every
+// peer access to this rank's memory goes through this GPU's L2), then ONE
+// thread releases a flag with st.release.sys, whose cumulativity orders every
+// write it has observed -- including its own stores into peer mailboxes --
+// before the flag.  Readers acquire the flag with ld.acquire.sys.  No
+// system-scope fence (MEMBAR.SYS) is taken on the hot path.
+__device__ __forceinline__ void dist_fence() { __threadfence(); }
+
 __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
   return *reinterpret_cast<const volatile unsigned long long*>(p);
 }
@@ -63,26 +71,21 @@ __global__ void dist_put_kernel(DistDev D, int phase, int slot, const double* __
   const unsigned long long s = ld_volatile_u64(D.seq + phase);
   const int64_t par = (int64_t)((s + 1) & 1);
   const int64_t total = D.send_off[D.nnbr];
+  // pack into this rank's own send buffer (the peers pull it)
+  double* sb = D.sendb + (slot * 2 + par) * D.send_total;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int qi = 0;
-    while (i >= D.send_off[qi + 1]) ++qi;
-    const int q = D.nbr[qi];
-    double* dst = D.precv[q] + (slot * 2 + par) * D.precv_total[q] + D.pbase_for_me[q] +
-                  (i - D.send_off[qi]);
-    *dst = w[D.send_idx[i]];
-  }
-  __threadfence_system();
+       i += (int64_t)gridDim.x * blockDim.x)
+    sb[i] = w[D.send_idx[i]];
+  dist_fence();
   __syncthreads();
   if (threadIdx.x == 0) last = atomicAdd(D.counter + phase, 1u) == gridDim.x - 1;
   __syncthreads();
   if (!last || threadIdx.x != 0) return;
-  __threadfence_system();
+  dist_fence();
   D.counter[phase] = 0;
   for (int q = 0; q < D.nranks; ++q)
     for (int c = 0; c < nscal; ++c)
       D.pmbox[q][mbox_index(phase, (int)par, D.rank, c)] = scal[c];
-  __threadfence_system();
   for (int q = 0; q < D.nranks; ++q)
     if (q != D.rank) st_release_sys(D.pflags[q] + phase * kMaxRanks + D.rank, s + 1);
   D.seq[phase] = s + 1;
@@ -130,7 +133,12 @@ __global__ void dist_iface_kernel(DistDev D, int phase, int slot, double* __rest
     }
   }
   const int64_t par = (int64_t)(ld_volatile_u64(D.seq + phase) & 1);
-  const double* rb = D.recv + (slot * 2 + par) * D.recv_total;
+  // remote copies are pulled from the owners' send buffers over NVLink
+  const double* src[kMaxRanks];
+  for (int qi = 0; qi < D.nnbr; ++qi) {
+    const int q = D.nbr[qi];
+    src[qi] = D.psend[q] + (slot * 2 + par) * D.psend_total[q] + D.pbase_from[q];
+  }
   const int64_t NL = D.nodes_local;
   for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < D.n_if;
        g += (int64_t)gridDim.x * blockDim.x) {
@@ -138,7 +146,16 @@ __global__ void dist_iface_kernel(DistDev D, int phase, int slot, double* __rest
     double sum = 0.0;
     for (int c = lo; c < hi; ++c) {
       const int32_t code = D.if_code[c];
-      sum += code >= NL ? __ldcv(rb + (code - NL)) : f[code < 0 ? ~code : code];
+      double v;
+      if (code >= NL) {
+        const int64_t rpos = code - NL;
+        int qi = 0;
+        while (rpos >= D.recv_base[qi + 1]) ++qi;
+        v = __ldcv(src[qi] + (rpos - D.recv_base[qi]));
+      } else {
+        v = f[code < 0 ? ~code : code];
+      }
+      sum += v;
     }
     for (int c = lo; c < hi; ++c) {
       const int32_t code = D.if_code[c];
@@ -159,7 +176,6 @@ __global__ void dist_allreduce_kernel(DistDev D, int phase, const double* __rest
   for (int q = 0; q < D.nranks; ++q)
     for (int c = 0; c < count; ++c)
       D.pmbox[q][mbox_index(phase, (int)((s + 1) & 1), D.rank, c)] = in[c];
-  __threadfence_system();
   for (int q = 0; q < D.nranks; ++q)
     if (q != D.rank) st_release_sys(D.pflags[q] + phase * kMaxRanks + D.rank, s + 1);
   D.seq[phase] = s + 1;
@@ -184,7 +200,6 @@ __device__ void dist_scalar_step(const DistDev& D, CgScalars* __restrict__ sc, d
   for (int q = 0; q < D.nranks; ++q)
     for (int c = 0; c < 2; ++c)
       D.pmbox[q][mbox_index(phase, (int)((s + 1) & 1), D.rank, c)] = mine[c];
-  __threadfence_system();
   for (int q = 0; q < D.nranks; ++q)
     if (q != D.rank) st_release_sys(D.pflags[q] + phase * kMaxRanks + D.rank, s + 1);
   D.seq[phase] = s + 1;
@@ -225,26 +240,21 @@ __device__ void dist_scalar_step(const DistDev& D, CgScalars* __restrict__ sc, d
 }
 
 // Sends of one element-step from the Ax epilogue: the group's threads store
-// the interface values of its element(s) straight into the neighbours'
-// receive buffers (phase 0), then fence at system scope.  Called by every
+// the interface values of its element(s) into this rank's send buffer
+// (phase 0, neighbour-major blocks pulled by the peers).  Called by every
 // thread of a consumer group; group-uniform control flow.
 __device__ __forceinline__ void dist_send_elements(const DistDev* __restrict__ D, int par,
                                                    const double* __restrict__ w, int64_t e0,
                                                    int cnt, int n3, int lt, int tg) {
-  bool stored = false;
+  // (published by the last-CTA ticket's fence, released by
+  // dist_release_phase0)
+  double* sb = D->sendb + (int64_t)par * D->send_total;  // slot 0 (the CG loop)
   for (int el = 0; el < cnt; ++el) {
     const int64_t e = e0 + el;
     const int lo = D->esend_off[e], hi = D->esend_off[e + 1];
-    for (int c = lo + lt; c < hi; c += tg) {
-      const int qi = D->esend_q[c];
-      const int q = D->nbr[qi];
-      double* dst = D->precv[q] + (int64_t)par * D->precv_total[q] + D->pbase_for_me[q] +
-                    D->esend_pos[c];
-      *dst = w[e * n3 + D->esend_node[c]];
-      stored = true;
-    }
+    for (int c = lo + lt; c < hi; c += tg)
+      sb[D->send_off[D->esend_q[c]] + D->esend_pos[c]] = w[e * n3 + D->esend_node[c]];
   }
-  if (stored) __threadfence_system();
 }
 
 // Release of phase 0 by the last CTA of K1 (one thread): this rank's p'Ap
@@ -252,9 +262,7 @@ __device__ __forceinline__ void dist_send_elements(const DistDev* __restrict__ D
 __device__ void dist_release_phase0(const DistDev& D, double pq_loc) {
   const unsigned long long s = ld_volatile_u64(D.seq);
   const int par = (int)((s + 1) & 1);
-  __threadfence_system();
   for (int q = 0; q < D.nranks; ++q) D.pmbox[q][mbox_index(0, par, D.rank, 0)] = pq_loc;
-  __threadfence_system();
   for (int q = 0; q < D.nranks; ++q)
     if (q != D.rank) st_release_sys(D.pflags[q] + D.rank, s + 1);
   D.seq[0] = s + 1;

@@ -70,12 +70,14 @@ struct CgScalars {
 // ---- multi-GPU peer windows ------------------------------------------------
 constexpr int kMaxRanks = 8;
 // Window layout (bytes): flags [4 phases][kMaxRanks] u64 at 0, mailboxes
-// [4 phases][2 parities][kMaxRanks][4] f64 at 256, receive buffers
-// [2 slots][2 parities][recv_total] f64 at 2304.  Phases: 0 halo+p'Ap in the
+// [4 phases][2 parities][kMaxRanks][4] f64 at 256, SEND buffers
+// [2 slots][2 parities][send_total] f64 at 2304.  Phases: 0 halo+p'Ap in the
 // CG loop, 1 r'z/r'r, 2 standalone gather-scatter halo, 3 setup reductions.
-// Parity = sequence number & 1: a peer can run at most one use of a phase
-// ahead (it needs this rank's flag of the previous use), so double buffering
-// makes every read race-free.
+// The halo is PULLED: a rank writes its interface copy values into its own
+// send buffer (neighbour-major blocks), releases its flag, and the peers read
+// the blocks over NVLink.  Parity = sequence number & 1: a peer can run at most
+// one use of a phase ahead (it needs this rank's flag of the previous use), so
+// double buffering makes every access race-free.
 constexpr size_t kWinFlags = 0, kWinMbox = 256, kWinRecv = 2304;
 
 __host__ __device__ constexpr int mbox_index(int phase, int par, int src, int c) {
@@ -87,16 +89,18 @@ struct DistDev {
   int64_t nodes_local = 0;
   unsigned long long* flags = nullptr;  // my window
   double* mbox = nullptr;
-  double* recv = nullptr;
+  double* sendb = nullptr;              // my send buffer [2 slots][2 par][send_total]
   int64_t recv_total = 0;
+  int64_t send_total = 0;
   unsigned long long* pflags[kMaxRanks] = {};  // peer windows (own rank: mine)
   double* pmbox[kMaxRanks] = {};
-  double* precv[kMaxRanks] = {};
-  int64_t precv_total[kMaxRanks] = {};
-  int64_t pbase_for_me[kMaxRanks] = {};  // my block's offset in peer q's receive buffer
+  double* psend[kMaxRanks] = {};
+  int64_t psend_total[kMaxRanks] = {};
+  int64_t pbase_from[kMaxRanks] = {};  // offset of peer q's block destined to me
   int nnbr = 0;
   int nbr[kMaxRanks] = {};
   int64_t send_off[kMaxRanks + 1] = {};
+  int64_t recv_base[kMaxRanks + 1] = {};  // per neighbour index, + total
   const int32_t* send_idx = nullptr;
   int64_t n_if = 0;
   const int32_t* if_off = nullptr;
@@ -111,6 +115,7 @@ struct DistDev {
   unsigned long long* seq = nullptr;  // device [4]
   unsigned int* counter = nullptr;    // device [4]
   int* status = nullptr;              // device: 1 on exchange timeout
+  int debug_nosend = 0;               // SBX_DEBUG_NOSEND: skip halo sends (timing only)
 };
 
 // distributed gather-scatter of a local field (halo exchange over the peer
