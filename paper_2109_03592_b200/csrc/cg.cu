@@ -565,50 +565,121 @@ __global__ void __launch_bounds__(AxCfg<n>::threads)
 }
 
 // --------------------------------------------- K2 (TMA pipeline, box) -----
-// Same math as cg_update_box_kernel, but the element's own w, r, 1/diag
-// columns are streamed into shared memory by a producer warp with 1-D TMA
-// bulk copies (ring of slots owned per consumer group, as in ax_tma_kernel),
-// so HBM latency is hidden by the ring and registers stay free for the
-// partner-copy gathers, which hit L2.  The producer warp also writes, per
-// element of a slot, its 27-neighbourhood (lane l: neighbour (l%3-1,
-// l/3%3-1, l/9-1) as a local element id, -1 outside the domain = Dirichlet
-// face, -2 on another rank), so the consumers do no index arithmetic.
+// Same math as cg_update_box_kernel, fed from shared memory.  A producer warp
+// streams the element's own w, r, 1/diag columns with 1-D TMA bulk copies
+// (ring of slots owned per consumer group, as in ax_tma_kernel) and writes,
+// per element of a slot, its 27-neighbourhood codes (lane l: neighbour
+// (l%3-1, l/3%3-1, l/9-1) as a local element id, -1 outside the domain =
+// Dirichlet face, -2 on another rank), released on a separate metadata
+// barrier.  The partner copies a column needs (x, y, xy columns and the
+// z-face values of the elements below / above) are gathered by each consumer
+// thread with per-thread async copies (cp.async, 8 bytes, zero-filled when
+// absent) into a double-buffered staging area ONE group-step AHEAD, so the L2
+// latency of the gathers overlaps the previous step's arithmetic.
+template <int n>
+struct K2Stage {
+  static constexpr int N = n - 1;
+  // staged values of column (i, j): x, y, xy partner columns (n each) and,
+  // per z face, the own / x / y / xy partners' face values
+  __host__ __device__ static constexpr int count(int i, int j) {
+    const int xs = (i == 0 || i == N), ys = (j == 0 || j == N);
+    return n * (xs + ys + xs * ys) + 2 * (1 + xs + ys + xs * ys);
+  }
+  __host__ __device__ static constexpr int offset(int ij) {
+    int o = 0;
+    for (int q = 0; q < ij; ++q) o += count(q % n, q / n);
+    return o;
+  }
+  static constexpr int PER_ELEM = ((offset(n * n) + 1) / 2) * 2;  // doubles
+};
+
 template <int n, int GROUPS, int SPG>
 struct K2Layout {
   using T = TmaGeom<n>;
   static constexpr int V_D = ((T::EPG * T::n3 + 1) / 2) * 2 + 2;
   static constexpr int SLOT_D = 3 * V_D;
   static constexpr int S = GROUPS * SPG;
+  static constexpr int STG_D = T::EPG * K2Stage<n>::PER_ELEM;  // one staging buffer
   static constexpr size_t BAR_BYTES = ((2 * S * 8 + 127) / 128) * 128;  // full[S] + empty[S]
-  static constexpr size_t META_BYTES = (size_t)S * T::EPG * 32 * 4;
-  static constexpr size_t smem = BAR_BYTES + META_BYTES + sizeof(double) * (size_t)S * SLOT_D;
+  static constexpr size_t META_BYTES = (((size_t)GROUPS * 2 * T::EPG * 32 * 4 + 127) / 128) * 128;
+  static constexpr size_t smem = BAR_BYTES + META_BYTES +
+                                 sizeof(double) * ((size_t)S * SLOT_D + (size_t)GROUPS * 2 * STG_D);
   static constexpr int threads = GROUPS * T::TG + 32;
 };
 
 template <int n>
 struct K2Choice {
   using T = TmaGeom<n>;
-  static constexpr size_t slot_bytes =
-      sizeof(double) * K2Layout<n, 1, 1>::SLOT_D + (size_t)T::EPG * 32 * 4;
+  using L1 = K2Layout<n, 1, 1>;
+  static constexpr size_t BUDGET = 225 * 1024 - 512;
+  static constexpr size_t slot_bytes = sizeof(double) * L1::SLOT_D + 16;
+  static constexpr size_t group_bytes = sizeof(double) * 2 * L1::STG_D + 2 * T::EPG * 32 * 4;
   static constexpr int pick() {
     for (int g = 16; g >= 1; --g) {
       if (g * T::TG + 32 > 1024) continue;
       if (g * T::TG > 384) continue;  // ~150 registers per consumer thread
-      if (256 + (size_t)g * 2 * slot_bytes <= 225 * 1024) return g;
+      if ((size_t)g * (2 * slot_bytes + group_bytes) <= BUDGET) return g;
     }
     return 1;
   }
   static constexpr int GROUPS = pick();
   static constexpr int spg() {
-    const int p = (int)((225 * 1024 - 384) / (GROUPS * slot_bytes));
+    const size_t rest = BUDGET - (size_t)GROUPS * group_bytes;
+    const int p = (int)(rest / (GROUPS * slot_bytes));
     return p > 4 ? 4 : p;
   }
   static constexpr int SPG = spg();
+  static constexpr bool ok = (size_t)GROUPS * (2 * slot_bytes + group_bytes) <= BUDGET;
 };
 
 // neighbour code: >= 0 local element, -1 outside (Dirichlet), -2 other rank,
 // -3 the node is not on that face (no partner)
 __device__ __forceinline__ bool nb_act(int c) { return c >= 0 || c == -2; }
+
+// 8-byte asynchronous global -> shared copy; zero-filled when !valid
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(valid ? 8 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int K>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(K) : "memory");
+}
+
+// A column's view of its element's neighbourhood (from the slot metadata).
+struct ColNb {
+  int lx, ly, lxy, z[2], zx[2], zy[2], zxy[2];
+  bool rem_xy, rem_z[2];
+};
+
+template <bool TABLE>
+__device__ __forceinline__ ColNb col_nb(const int32_t* nb, int xi, int yi, bool xs, bool ys) {
+  ColNb c;
+  c.lx = xs ? nb[xi + 12] : -3;
+  c.ly = ys ? nb[1 + 3 * yi + 9] : -3;
+  c.lxy = (xs && ys) ? nb[xi + 3 * yi + 9] : -3;
+#pragma unroll
+  for (int f = 0; f < 2; ++f) {
+    const int zo = f == 0 ? 0 : 18;
+    c.z[f] = nb[4 + zo];
+    c.zx[f] = xs ? nb[xi + 3 + zo] : -3;
+    c.zy[f] = ys ? nb[1 + 3 * yi + zo] : -3;
+    c.zxy[f] = (xs && ys) ? nb[xi + 3 * yi + zo] : -3;
+  }
+  c.rem_xy = false;
+  c.rem_z[0] = c.rem_z[1] = false;
+  if constexpr (TABLE) {
+    c.rem_xy = c.lx == -2 || c.ly == -2 || c.lxy == -2;
+#pragma unroll
+    for (int f = 0; f < 2; ++f)
+      c.rem_z[f] = c.rem_xy || c.z[f] == -2 || c.zx[f] == -2 || c.zy[f] == -2 || c.zxy[f] == -2;
+  }
+  return c;
+}
 
 template <int n, int GROUPS, int SPG, bool TABLE>
 __global__ void __launch_bounds__(K2Layout<n, GROUPS, SPG>::threads, 1)
@@ -620,6 +691,7 @@ __global__ void __launch_bounds__(K2Layout<n, GROUPS, SPG>::threads, 1)
                          cudaGraphConditionalHandle cond, int use_cond) {
   using T = TmaGeom<n>;
   using L = K2Layout<n, GROUPS, SPG>;
+  using St = K2Stage<n>;
   constexpr int S = L::S;
   constexpr int N = n - 1;
   constexpr int EPG = T::EPG;
@@ -633,13 +705,14 @@ __global__ void __launch_bounds__(K2Layout<n, GROUPS, SPG>::threads, 1)
   const double alpha = sc->alpha;
   uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
   uint64_t* empty = full + S;
-  int32_t* meta = reinterpret_cast<int32_t*>(smraw + L::BAR_BYTES);  // [S][EPG][32]
+  int32_t* meta = reinterpret_cast<int32_t*>(smraw + L::BAR_BYTES);  // [GROUPS][2][EPG][32]
   double* slots = reinterpret_cast<double*>(smraw + L::BAR_BYTES + L::META_BYTES);
+  double* stage = slots + (size_t)S * L::SLOT_D;  // [GROUPS][2][STG_D]
   const int64_t NG = (E + EPG - 1) / EPG;
   const int64_t M = NG > (int64_t)blockIdx.x ? (NG - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 32);  // every producer lane arrives (meta), lane 0 with the bytes
+      mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     mbar_fence_init();
@@ -648,18 +721,52 @@ __global__ void __launch_bounds__(K2Layout<n, GROUPS, SPG>::threads, 1)
   double rz = 0.0, rr = 0.0;
   const int warp = threadIdx.x >> 5;
   if (warp == GROUPS * T::TG / 32) {
-    // ---------------- producer warp --------------------------------------
-    const int lane = threadIdx.x & 31;
-    const int dx = lane % 3 - 1, dy = (lane / 3) % 3 - 1, dz = lane / 9 - 1;
-    // neighbour `lane` of element e (box lattice, or this rank's table)
-    auto nb_of = [&](int64_t e) -> int32_t {
-      if (lane >= 27 || e >= E) return -1;
+    // ---------------- producer warp: one lane drives the TMA ring --------
+    if ((threadIdx.x & 31) == 0) {
+      for (int64_t m = 0; m < M; ++m) {
+        const int s = (int)(m % S);
+        if (m >= S) mbar_wait(&empty[s], (uint32_t)((m / S - 1) & 1));
+        const int64_t e0 = (blockIdx.x + m * gridDim.x) * EPG;
+        const int64_t cnt = (E - e0) < EPG ? (E - e0) : EPG;
+        const int shift = (int)((e0 * T::n3) & 1);
+        const uint32_t vb = (uint32_t)((((cnt * T::n3 + shift) * 8) + 15) / 16 * 16);
+        double* slot = slots + s * L::SLOT_D;
+        mbar_expect_tx(&full[s], (dinv ? 3 : 2) * vb);
+        tma_load_1d(slot, w + e0 * T::n3 - shift, vb, &full[s]);
+        tma_load_1d(slot + L::V_D, r + e0 * T::n3 - shift, vb, &full[s]);
+        if (dinv) tma_load_1d(slot + 2 * L::V_D, dinv + e0 * T::n3 - shift, vb, &full[s]);
+      }
+    }
+  } else {
+    // ---------------- consumer groups ------------------------------------
+    const int g = threadIdx.x / T::TG, lt = threadIdx.x % T::TG;
+    const int sl = lt / T::nn, ij = lt % T::nn, i = ij % n, j = ij / n;
+    const bool act = sl < EPG;
+    // thread constants: the x / y face the column (i, j) lies on, its partner
+    // columns' local indices and its staging slots
+    const int xi = i == 0 ? 0 : (i == N ? 2 : 1), yi = j == 0 ? 0 : (j == N ? 2 : 1);
+    const bool xs = xi != 1, ys = yi != 1, xys = xs && ys;
+    const int cxo = j * n + (N - i), cyo = (N - j) * n + i, cxyo = (N - j) * n + (N - i);
+    const int so = sl * St::PER_ELEM + (act ? St::offset(ij) : 0);
+    const int ox = 0, oy = xs ? n : 0, oxy = oy + (ys ? n : 0), oz = oxy + (xys ? n : 0);
+    const int zc = 1 + xs + ys + xys;  // staged values per z face
+    double* stg = stage + (size_t)g * 2 * L::STG_D;
+    // the group's neighbourhood codes, double-buffered like the staging:
+    // entry q = neighbour q % 32 of element q / 32 of a step
+    int32_t* gmeta = meta + g * 2 * EPG * 32;
+    constexpr int NQ = (EPG * 32 + T::TG - 1) / T::TG;
+    auto code_of = [&](int64_t mm, int q) -> int32_t {
+      const int d = q % 32;
+      const int64_t ee = (blockIdx.x + mm * gridDim.x) * EPG + q / 32;
+      if (d >= 27 || q >= EPG * 32 || mm >= M || ee >= E) return -1;
       if constexpr (TABLE) {
-        return __ldg(nbr27 + e * 27 + lane);
+        return __ldg(nbr27 + ee * 27 + d);
       } else {
-        const uint32_t ue = (uint32_t)e, uex = (uint32_t)bx.ex, uey = (uint32_t)bx.ey;
-        const uint32_t q = ue / uex;
-        int x = (int)(ue - q * uex) + dx, y = (int)(q % uey) + dy, z = (int)(q / uey) + dz;
+        if (bx.dbg) return -3;  // timing experiment only: no partners
+        const int dx = d % 3 - 1, dy = (d / 3) % 3 - 1, dz = d / 9 - 1;
+        const uint32_t ue = (uint32_t)ee, uex = (uint32_t)bx.ex, uey = (uint32_t)bx.ey;
+        const uint32_t qq = ue / uex;
+        int x = (int)(ue - qq * uex) + dx, y = (int)(qq % uey) + dy, z = (int)(qq / uey) + dz;
         if (x < 0 || x >= bx.ex) {
           if (!bx.px) return -1;
           x = x < 0 ? bx.ex - 1 : 0;
@@ -675,107 +782,121 @@ __global__ void __launch_bounds__(K2Layout<n, GROUPS, SPG>::threads, 1)
         return (int32_t)(x + bx.ex * (y + bx.ey * z));
       }
     };
-    int32_t nxt[EPG];  // loaded one step ahead (table mode: hides the load)
-    if (M > 0) {
+    // table mode: the codes of the step after next ride in registers so the
+    // table load overlaps a whole step
+    int32_t pre[NQ];
+    auto fill = [&](int64_t mm, int b) {
 #pragma unroll
-      for (int el = 0; el < EPG; ++el) nxt[el] = nb_of((int64_t)blockIdx.x * EPG + el);
-    }
-    for (int64_t m = 0; m < M; ++m) {
-      const int s = (int)(m % S);
-      if (m >= S) mbar_wait(&empty[s], (uint32_t)((m / S - 1) & 1));
-      const int64_t e0 = (blockIdx.x + m * gridDim.x) * EPG;
-      if (lane == 0) {
-        const int64_t cnt = (E - e0) < EPG ? (E - e0) : EPG;
-        const int shift = (int)((e0 * T::n3) & 1);
-        const uint32_t vb = (uint32_t)((((cnt * T::n3 + shift) * 8) + 15) / 16 * 16);
-        double* slot = slots + s * L::SLOT_D;
-        mbar_expect_tx(&full[s], (dinv ? 3 : 2) * vb);
-        tma_load_1d(slot, w + e0 * T::n3 - shift, vb, &full[s]);
-        tma_load_1d(slot + L::V_D, r + e0 * T::n3 - shift, vb, &full[s]);
-        if (dinv) tma_load_1d(slot + 2 * L::V_D, dinv + e0 * T::n3 - shift, vb, &full[s]);
+      for (int t = 0; t < NQ; ++t) {
+        const int q = lt + t * T::TG;
+        const int32_t v = TABLE ? pre[t] : code_of(mm, q);
+        if (q < EPG * 32) gmeta[b * EPG * 32 + q] = v;
+        if (TABLE) pre[t] = code_of(mm + GROUPS, q);
       }
+    };
+    // issue the gathers of step mm into staging buffer b (group-uniform call;
+    // the step's codes are in gmeta[b])
+    auto issue = [&](int64_t mm, int b) {
+      const int64_t e = (blockIdx.x + mm * gridDim.x) * EPG + sl;
+      if (act && e < E) {
+        const ColNb c = col_nb<TABLE>(gmeta + (b * EPG + sl) * 32, xi, yi, xs, ys);
+        double* d = stg + b * L::STG_D + so;
+        const double* px = w + (int64_t)(c.lx < 0 ? 0 : c.lx) * T::n3 + cxo;
+        const double* py = w + (int64_t)(c.ly < 0 ? 0 : c.ly) * T::n3 + cyo;
+        const double* pxy = w + (int64_t)(c.lxy < 0 ? 0 : c.lxy) * T::n3 + cxyo;
 #pragma unroll
-      for (int el = 0; el < EPG; ++el) meta[(s * EPG + el) * 32 + lane] = nxt[el];
-      if (lane != 0) mbar_arrive(&full[s]);
-      if (m + 1 < M) {
-        const int64_t e1 = (blockIdx.x + (m + 1) * gridDim.x) * EPG;
+        for (int k = 0; k < n; ++k) {
+          const bool rk = k == 0 ? c.rem_z[0] : (k == N ? c.rem_z[1] : c.rem_xy);
+          if (xs) cp_async8(d + ox + k, px + k * T::nn, c.lx >= 0 && !rk);
+          if (ys) cp_async8(d + oy + k, py + k * T::nn, c.ly >= 0 && !rk);
+          if (xys) cp_async8(d + oxy + k, pxy + k * T::nn, c.lxy >= 0 && !rk);
+        }
 #pragma unroll
-        for (int el = 0; el < EPG; ++el) nxt[el] = nb_of(e1 + el);
+        for (int f = 0; f < 2; ++f) {
+          // plane N of the element below (f = 0) / plane 0 of the one above
+          const int64_t ko = f == 0 ? (int64_t)N * T::nn : 0;
+          const bool rk = c.rem_z[f];
+          double* dz = d + oz + f * zc;
+          cp_async8(dz, w + (int64_t)(c.z[f] < 0 ? 0 : c.z[f]) * T::n3 + ko + ij,
+                    c.z[f] >= 0 && !rk);
+          int q = 1;
+          if (xs)
+            cp_async8(dz + q++, w + (int64_t)(c.zx[f] < 0 ? 0 : c.zx[f]) * T::n3 + ko + cxo,
+                      c.zx[f] >= 0 && !rk);
+          if (ys)
+            cp_async8(dz + q++, w + (int64_t)(c.zy[f] < 0 ? 0 : c.zy[f]) * T::n3 + ko + cyo,
+                      c.zy[f] >= 0 && !rk);
+          if (xys)
+            cp_async8(dz + q, w + (int64_t)(c.zxy[f] < 0 ? 0 : c.zxy[f]) * T::n3 + ko + cxyo,
+                      c.zxy[f] >= 0 && !rk);
+        }
       }
+      cp_async_commit();
+    };
+    if (g < M) {
+      if (TABLE) {
+#pragma unroll
+        for (int t = 0; t < NQ; ++t) pre[t] = code_of(g, lt + t * T::TG);
+      }
+      fill(g, 0);
+      named_bar_sync(1 + g, T::TG);
+      issue(g, 0);
     }
-  } else {
-    // ---------------- consumer groups ------------------------------------
-    const int g = threadIdx.x / T::TG, lt = threadIdx.x % T::TG;
-    const int sl = lt / T::nn, ij = lt % T::nn, i = ij % n, j = ij / n;
-    const bool act = sl < EPG;
-    // thread constants: which x / y face the column (i, j) lies on
-    const int xi = i == 0 ? 0 : (i == N ? 2 : 1), yi = j == 0 ? 0 : (j == N ? 2 : 1);
-    const bool xs = xi != 1, ys = yi != 1;
-    const int cxo = j * n + (N - i), cyo = (N - j) * n + i, cxyo = (N - j) * n + (N - i);
     for (int64_t m = g; m < M; m += GROUPS) {
       const int s = (int)(m % S);
+      const int b = (int)((m / GROUPS) & 1);
+      const bool more = m + GROUPS < M;
+      if (more) {
+        fill(m + GROUPS, b ^ 1);
+        named_bar_sync(1 + g, T::TG);
+        issue(m + GROUPS, b ^ 1);
+      }
       const int64_t e = (blockIdx.x + m * gridDim.x) * EPG + sl;
       const bool valid = act && e < E;
       mbar_wait(&full[s], (uint32_t)((m / S) & 1));
+      if (more)
+        cp_async_wait<1>();
+      else
+        cp_async_wait<0>();
       if (valid) {
-        const int32_t* nb = meta + (s * EPG + sl) * 32;
-        auto at = [&](int a, int b, int c) { return nb[a + 3 * b + 9 * c]; };
-        const int lx = xs ? at(xi, 1, 1) : -3, ly = ys ? at(1, yi, 1) : -3;
-        const int lxy = (xs && ys) ? at(xi, yi, 1) : -3;
-        const int z0 = at(1, 1, 0), zN = at(1, 1, 2);
-        const int z0x = xs ? at(xi, 1, 0) : -3, zNx = xs ? at(xi, 1, 2) : -3;
-        const int z0y = ys ? at(1, yi, 0) : -3, zNy = ys ? at(1, yi, 2) : -3;
-        const int z0xy = (xs && ys) ? at(xi, yi, 0) : -3, zNxy = (xs && ys) ? at(xi, yi, 2) : -3;
-        const bool ax = nb_act(lx), ay = nb_act(ly), az0 = nb_act(z0), azN = nb_act(zN);
-        const bool mxy = lx == -1 || ly == -1;
-        const bool m0 = z0 == -1, mN = zN == -1;
-        // interface nodes (a copy on another rank) were assembled by
-        // dist_iface_kernel: own value only
-        bool rem_xy = false, rem_z0 = false, rem_zN = false;
-        if constexpr (TABLE) {
-          rem_xy = lx == -2 || ly == -2 || lxy == -2;
-          rem_z0 = rem_xy || z0 == -2 || z0x == -2 || z0y == -2 || z0xy == -2;
-          rem_zN = rem_xy || zN == -2 || zNx == -2 || zNy == -2 || zNxy == -2;
-        }
-        // partner-copy gathers (L2): x, y, xy columns and the z-face rows
-        double wx[n], wy[n], wxy[n];
-        const double* px = w + (int64_t)(lx < 0 ? 0 : lx) * T::n3 + cxo;
-        const double* py = w + (int64_t)(ly < 0 ? 0 : ly) * T::n3 + cyo;
-        const double* pxy = w + (int64_t)(lxy < 0 ? 0 : lxy) * T::n3 + cxyo;
+        const ColNb c = col_nb<TABLE>(gmeta + (b * EPG + sl) * 32, xi, yi, xs, ys);
+        const double* d = stg + b * L::STG_D + so;
+        const bool ax = nb_act(c.lx), ay = nb_act(c.ly);
+        const bool az0 = nb_act(c.z[0]), azN = nb_act(c.z[1]);
+        const bool mxy = c.lx == -1 || c.ly == -1;
+        const bool m0 = c.z[0] == -1, mN = c.z[1] == -1;
+        double zs[2];
 #pragma unroll
-        for (int k = 0; k < n; ++k) {
-          const bool rk = k == 0 ? rem_z0 : (k == N ? rem_zN : rem_xy);
-          wx[k] = (lx >= 0 && !rk) ? __ldg(px + k * T::nn) : 0.0;
-          wy[k] = (ly >= 0 && !rk) ? __ldg(py + k * T::nn) : 0.0;
-          wxy[k] = (lxy >= 0 && !rk) ? __ldg(pxy + k * T::nn) : 0.0;
+        for (int f = 0; f < 2; ++f) {
+          const double* dz = d + oz + f * zc;
+          const double q0 = dz[0];
+          const double q1 = xs ? dz[1] : 0.0;
+          const double q2 = ys ? dz[1 + xs] : 0.0;
+          const double q3 = xys ? dz[3] : 0.0;
+          zs[f] = (q0 + q1) + (q2 + q3);
         }
-        auto zld = [&](int l, int off, bool rk) {
-          return (l >= 0 && !rk) ? __ldg(w + (int64_t)l * T::n3 + off) : 0.0;
-        };
-        // plane N of the element below / plane 0 of the element above
-        const double a0 = zld(z0, N * T::nn + ij, rem_z0), a1 = zld(z0x, N * T::nn + cxo, rem_z0);
-        const double a2 = zld(z0y, N * T::nn + cyo, rem_z0);
-        const double a3 = zld(z0xy, N * T::nn + cxyo, rem_z0);
-        const double b0 = zld(zN, ij, rem_zN), b1 = zld(zNx, cxo, rem_zN);
-        const double b2 = zld(zNy, cyo, rem_zN), b3 = zld(zNxy, cxyo, rem_zN);
-        const double zs0 = (a0 + a1) + (a2 + a3), zsN = (b0 + b1) + (b2 + b3);
         const double wgt_xy = (ax ? 0.5 : 1.0) * (ay ? 0.5 : 1.0);
         const int shift = (int)(((e - sl) * T::n3) & 1);
-        const double* slot = slots + s * L::SLOT_D + shift + sl * T::n3 + ij;
+        const double* own = slots + s * L::SLOT_D + shift + sl * T::n3 + ij;
         double* rp = r + e * T::n3 + ij;
 #pragma unroll
         for (int k = 0; k < n; ++k) {
-          const double wo = slot[k * T::nn];
-          const double ro = slot[L::V_D + k * T::nn];
-          const double dv = dinv ? slot[2 * L::V_D + k * T::nn] : 1.0;
+          const double wo = own[k * T::nn];
+          const double ro = own[L::V_D + k * T::nn];
+          const double dv = dinv ? own[2 * L::V_D + k * T::nn] : 1.0;
+          const double wx = xs ? d[ox + k] : 0.0;
+          const double wy = ys ? d[oy + k] : 0.0;
+          const double wxy = xys ? d[oxy + k] : 0.0;
           // Pairwise tree over the copies: x-pairs, the y-pair of x-pairs,
           // then the z-pair of planes.  Each level adds exactly two operands
           // (an absent partner contributes +0.0 in the same position for
           // every copy) and IEEE addition is commutative, so every copy of a
-          // node gets the same bits with no ordering logic.
-          double sum = (wo + wx[k]) + (wy[k] + wxy[k]);
-          if (k == 0) sum = sum + zs0;
-          if (k == N) sum = sum + zsN;
+          // node gets the same bits with no ordering logic.  Interface nodes
+          // (a copy on another rank) were assembled by dist_iface_kernel;
+          // their partners were staged as zeros: own value only.
+          double sum = (wo + wx) + (wy + wxy);
+          if (k == 0) sum = sum + zs[0];
+          if (k == N) sum = sum + zs[1];
           const bool msk = mxy || (k == 0 && m0) || (k == N && mN);
           const double q = msk ? 0.0 : sum;
           const double wgt =
@@ -1013,7 +1134,7 @@ cudaError_t launch_k2(const OpDev& op, const double* w, double* r, const double*
   static const bool use_flat = std::getenv("SBX_K2_FLAT") != nullptr;
   static const bool no_tma = std::getenv("SBX_NO_TMA") != nullptr;
   if (op.box && !use_col && !use_flat && !no_tma && n % 2 == 0 && aligned16(w) &&
-      aligned16(r) && aligned16(dinv)) {
+      aligned16(r) && aligned16(dinv) && K2Choice<n>::ok) {
     using Ch = K2Choice<n>;
     using L = K2Layout<n, Ch::GROUPS, Ch::SPG>;
     auto kern = op.table ? cg_update_tma_kernel<n, Ch::GROUPS, Ch::SPG, true>
@@ -1030,7 +1151,8 @@ cudaError_t launch_k2(const OpDev& op, const double* w, double* r, const double*
     const int64_t NG = (op.E + TmaGeom<n>::EPG - 1) / TmaGeom<n>::EPG;
     int64_t grid = num_sms(dev);
     if (grid > NG) grid = NG;
-    BoxP bx{op.ex, op.ey, op.ez, op.per[0], op.per[1], op.per[2], 0};
+    static const int nogather = std::getenv("SBX_K2_NOGATHER") ? 1 : 0;
+    BoxP bx{op.ex, op.ey, op.ez, op.per[0], op.per[1], op.per[2], nogather};
     kern<<<(unsigned)grid, L::threads, L::smem, s>>>(w, r, dinv, op.E, bx, op.nbr27, op.dd, sc,
                                                      partials, hist, hist_cap, cond, use_cond);
     return cudaGetLastError();
@@ -1254,13 +1376,23 @@ int CgEngine::build_graph(const CgRun& run) {
   cudaGraph_t body = params.conditional.phGraph_out[0];
   CG_CUDA(cudaStreamBeginCaptureToGraph(run.stream, body, nullptr, nullptr, 0,
                                         cudaStreamCaptureModeRelaxed));
-  cudaError_t e1 = k1(op, r_, run.dinv, p_, run.x, w_, run.h1, run.h2, sc_, partials_,
-                      run.stream);
-  cudaError_t e2 =
-      run.dist ? dist_iteration_tail(op, *run.dist, w_, r_, run.dinv, sc_, partials_, hist_,
-                                     hist_len_, handle, 1, run.stream)
-               : k2(op, w_, r_, run.dinv, sc_, partials_, hist_, hist_len_, handle, 1,
-                    run.stream);
+  // The body holds kUnroll iterations: every kernel returns at once when the
+  // solve is done (sc->done), and the last K2 that ran sets the condition, so
+  // the loop still stops on the exact iteration; the while-node's per-body
+  // overhead is paid once per kUnroll iterations.
+  static const int kUnroll = [] {
+    const char* v = std::getenv("SBX_CG_UNROLL");
+    const int u = v ? std::atoi(v) : 4;
+    return u < 1 ? 1 : (u > 16 ? 16 : u);
+  }();
+  cudaError_t e1 = cudaSuccess, e2 = cudaSuccess;
+  for (int u = 0; u < kUnroll && e1 == cudaSuccess && e2 == cudaSuccess; ++u) {
+    e1 = k1(op, r_, run.dinv, p_, run.x, w_, run.h1, run.h2, sc_, partials_, run.stream);
+    e2 = run.dist ? dist_iteration_tail(op, *run.dist, w_, r_, run.dinv, sc_, partials_, hist_,
+                                        hist_len_, handle, 1, run.stream)
+                  : k2(op, w_, r_, run.dinv, sc_, partials_, hist_, hist_len_, handle, 1,
+                       run.stream);
+  }
   cudaGraph_t captured = nullptr;
   cudaError_t e3 = cudaStreamEndCapture(run.stream, &captured);
   CG_CUDA(e1);
