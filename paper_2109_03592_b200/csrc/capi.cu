@@ -562,6 +562,18 @@ sbx_status sbx_ctx_create(const sbx_problem_desc* desc, int device, sbx_ctx** ou
   return SBX_OK;
 }
 
+// Trilinear-element data for the fused CG kernel's on-the-fly metrics: the
+// per-element map coefficients and the GLL nodes / weights.
+sbx_status upload_trilinear(sbx_ctx* c, int degree, const double* corners, int64_t E) {
+  std::vector<double> tl(E * 24);
+  trilinear_coeffs(E, corners, tl.data());
+  double* dtl = nullptr;
+  SBX_TRY(dupload(c, &dtl, tl.data(), E * 24));
+  c->op.tl = dtl;
+  SBX_TRY(sbx_gll_basis(degree, c->op.Xh, c->op.Wh, nullptr));
+  return SBX_OK;
+}
+
 sbx_status sbx_ctx_create_box(const sbx_box_desc* d, int device, sbx_ctx** out) {
   if (!d || !out) {
     set_error("sbx_ctx_create_box: null argument");
@@ -584,8 +596,6 @@ sbx_status sbx_ctx_create_box(const sbx_box_desc* d, int device, sbx_ctx** out) 
   SBX_TRY(sbx_geometric_factors(E, d->degree, corners.data(), g[0].data(), g[1].data(),
                                 g[2].data(), g[3].data(), g[4].data(), g[5].data(), g[6].data(),
                                 nullptr, &bad));
-  corners.clear();
-  corners.shrink_to_fit();
   std::vector<int64_t> offsets(N + 1), nodes(N);
   int64_t G = 0;
   SBX_TRY(sbx_gather_scatter(d->ex, d->ey, d->ez, d->periodic, d->degree, nullptr,
@@ -603,6 +613,7 @@ sbx_status sbx_ctx_create_box(const sbx_box_desc* d, int device, sbx_ctx** out) 
   pd.group_offsets = offsets.data();
   pd.group_nodes = nodes.data();
   SBX_TRY(sbx_ctx_create(&pd, device, out));
+  SBX_TRY(upload_trilinear(*out, d->degree, corners.data(), E));
   // structured element-centric gather-scatter (needs >= 2 cells per periodic axis)
   const int counts[3] = {d->ex, d->ey, d->ez};
   bool ok = true;
@@ -943,6 +954,7 @@ sbx_status upload_dist(sbx_ctx* c, const DistPlan& P, const sbx_box_desc* d) {
     std::memcpy(&loc[le * 24], &all[P.loc_elems[le] * 24], 24 * sizeof(double));
   all.clear();
   all.shrink_to_fit();
+  SBX_TRY(upload_trilinear(c, d->degree, loc.data(), EL));
   std::vector<double> deriv(n * n);
   SBX_TRY(sbx_gll_basis(d->degree, nullptr, nullptr, deriv.data()));
   for (int q = 0; q < n * n; ++q) c->op.Dh[q] = deriv[q];

@@ -725,7 +725,7 @@ __global__ void __launch_bounds__(K2Layout<n, GROUPS, SPG>::threads, 1)
     if ((threadIdx.x & 31) == 0) {
       for (int64_t m = 0; m < M; ++m) {
         const int s = (int)(m % S);
-        if (m >= S) mbar_wait(&empty[s], (uint32_t)((m / S - 1) & 1));
+        if (m >= S) mbar_wait_backoff(&empty[s], (uint32_t)((m / S - 1) & 1));
         const int64_t e0 = (blockIdx.x + m * gridDim.x) * EPG;
         const int64_t cnt = (E - e0) < EPG ? (E - e0) : EPG;
         const int shift = (int)((e0 * T::n3) & 1);
@@ -1066,17 +1066,24 @@ int num_sms(int dev) {
   return g_num_sms[dev & 63];
 }
 
-template <int n, bool HAS_DINV, bool HAS_BM>
+// consumer groups of the TRI kernel, bounded by the register budget
+// (65536 / threads): the metric's per-column constants and temporaries
+constexpr int tri_max_groups(int n) { return n <= 8 ? 5 : (n <= 12 ? 2 : 1); }
+
+// TRI: the metric is formed at each node from the element's trilinear map
+// (op.tl) instead of streaming the 6 stored factors -- 48 fewer bytes per
+// node on an HBM-bound kernel, for ~50 more FP64 operations per node.
+template <int n, bool HAS_DINV, bool HAS_BM, bool TRI>
 cudaError_t launch_k1_tma(const OpDev& op, const double* r, const double* dinv, double* p,
                           double* x, double* w, double h1, double h2, CgScalars* sc,
                           double* partials, cudaStream_t s, int dev) {
   using Pol = CgK1Pol<HAS_DINV, HAS_BM>;
-  using Ch = TmaChoice<n, Pol::NV>;
+  using Ch = TmaChoice<n, Pol::NV, TRI, TRI ? tri_max_groups(n) : 8>;
   if constexpr (!Ch::ok) {
     return cudaErrorNotSupported;
   } else {
-    using L = TmaLayout<n, Pol::NV, Ch::GROUPS, Ch::S>;
-    auto kern = ax_tma_kernel<n, Pol, Ch::GROUPS, Ch::S>;
+    using L = TmaLayout<n, Pol::NV, Ch::GROUPS, Ch::S, TRI>;
+    auto kern = ax_tma_kernel<n, Pol, Ch::GROUPS, Ch::S, TRI>;
     static bool attr_set[64] = {};
     if (!attr_set[dev & 63]) {
       cudaError_t err =
@@ -1086,11 +1093,17 @@ cudaError_t launch_k1_tma(const OpDev& op, const double* r, const double* dinv, 
     }
     DParam<n> Dp;
     for (int q = 0; q < n * n; ++q) Dp.d[q] = op.Dh[q];
+    QParam<n> Qp;
+    for (int q = 0; q < n; ++q) {
+      Qp.x[q] = op.Xh[q];
+      Qp.w[q] = op.Wh[q];
+    }
     typename Pol::Args a{r, dinv, p, x, w, op.bm, h2, sc, op.dd, 0.0, 0.0, 0, 0, nullptr};
     const int64_t NG = (op.E + TmaGeom<n>::EPG - 1) / TmaGeom<n>::EPG;
     int64_t grid = num_sms(dev);
     if (grid > NG) grid = NG;
-    kern<<<(unsigned)grid, L::threads, L::smem, s>>>(a, op.G, op.E, h1, 1.0, Dp, partials);
+    kern<<<(unsigned)grid, L::threads, L::smem, s>>>(a, TRI ? op.tl : op.G, op.E, h1, 1.0, Dp,
+                                                     partials, Qp);
     return cudaGetLastError();
   }
 }
@@ -1106,10 +1119,16 @@ cudaError_t launch_k1(const OpDev& op, const double* r, const double* dinv, doub
   // only admissible K1 there
   if (op.dd && !k1_use_tma(op, r, dinv, p, x, h2)) return cudaErrorNotSupported;
   if (k1_use_tma(op, r, dinv, p, x, h2)) {
-    if (dinv && h2 != 0.0) return launch_k1_tma<n, true, true>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
-    if (dinv) return launch_k1_tma<n, true, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
-    if (h2 != 0.0) return launch_k1_tma<n, false, true>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
-    return launch_k1_tma<n, false, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
+    // trilinear elements (box contexts), Poisson / h2 = 0: on-the-fly metrics
+    static const bool stored = std::getenv("SBX_STORED_GEOMETRY") != nullptr;
+    const bool tri = op.tl && h2 == 0.0 && !stored && aligned16(op.tl);
+    if (dinv && h2 != 0.0) return launch_k1_tma<n, true, true, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
+    if (h2 != 0.0) return launch_k1_tma<n, false, true, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
+    if (dinv)
+      return tri ? launch_k1_tma<n, true, false, true>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev)
+                 : launch_k1_tma<n, true, false, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
+    return tri ? launch_k1_tma<n, false, false, true>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev)
+               : launch_k1_tma<n, false, false, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
   }
   static bool attr_set[64] = {};
   if (!attr_set[dev & 63]) {

@@ -41,6 +41,11 @@ struct OpDev {
   const int32_t* nbr27 = nullptr;
   const int64_t* gelem = nullptr;
   const DistDev* dd = nullptr;  // device copy of the exchange state (multi-GPU)
+  // trilinear elements (box contexts): per-element map coefficients [E][24]
+  // (see trilinear_coeffs) and the GLL nodes / weights, so the fused CG
+  // kernel can form the metric at each node instead of streaming G
+  const double* tl = nullptr;
+  double Xh[33], Wh[33];
 };
 
 // Device-resident CG scalars for the fused (FAST) solver.

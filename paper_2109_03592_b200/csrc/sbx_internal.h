@@ -28,5 +28,11 @@ int gather_scatter(int ex, int ey, int ez, const int* periodic, int degree, int6
                    int64_t* global_count);
 int dirichlet_mask(int ex, int ey, int ez, const int* periodic, int degree, double* mask);
 int partition_rcb(int64_t E, const double* corners, int ranks, int32_t* rank_of);
+// Coefficients of each element's trilinear map derivatives (on-the-fly
+// metrics of the fused CG kernel): tl[e][24] = S0, S1, S2, S01, S02, S12,
+// S012 (xyz each) and 3 pads, with
+//   dX/dr = S0 + S01 s + S02 t + S012 s t,  dX/ds = S1 + S01 r + S12 t + S012 r t,
+//   dX/dt = S2 + S02 r + S12 s + S012 r s.
+void trilinear_coeffs(int64_t E, const double* corners, double* tl);
 
 }  // namespace sbx

@@ -207,6 +207,26 @@ inline bool node_metric(const double* cr, double r, double s, double t, double w
 }
 }  // namespace
 
+// node_metric's Jacobian is sum_v X_v grad N_v with N_v = prod_q (1 + sg_q xi_q) / 2
+// (sg_q = +-1 from corner bit q); expanding the products gives the bilinear
+// forms of trilinear_coeffs, S_A = (1/8) sum_v (prod_{q in A} sg_q) X_v.
+void trilinear_coeffs(int64_t E, const double* corners, double* tl) {
+  host_parallel_for(E, [&](int64_t lo, int64_t hi) {
+    for (int64_t e = lo; e < hi; ++e) {
+      const double* cr = corners + e * 24;
+      double* o = tl + e * 24;
+      for (int q = 0; q < 24; ++q) o[q] = 0.0;
+      for (int v = 0; v < 8; ++v) {
+        const double s0 = (v & 1) ? 1.0 : -1.0, s1 = (v & 2) ? 1.0 : -1.0,
+                     s2 = (v & 4) ? 1.0 : -1.0;
+        const double sg[7] = {s0, s1, s2, s0 * s1, s0 * s2, s1 * s2, s0 * s1 * s2};
+        for (int a = 0; a < 7; ++a)
+          for (int p = 0; p < 3; ++p) o[a * 3 + p] += 0.125 * sg[a] * cr[v * 3 + p];
+      }
+    }
+  });
+}
+
 int geometric_factors(int64_t E, int degree, const double* corners, double* const g[6],
                       double* bm, double* jac, int64_t* bad_elem) {
   const int n = degree + 1;
