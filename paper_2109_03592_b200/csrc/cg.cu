@@ -1121,7 +1121,9 @@ cudaError_t launch_k1(const OpDev& op, const double* r, const double* dinv, doub
   if (k1_use_tma(op, r, dinv, p, x, h2)) {
     // trilinear elements (box contexts), Poisson / h2 = 0: on-the-fly metrics
     static const bool stored = std::getenv("SBX_STORED_GEOMETRY") != nullptr;
-    const bool tri = op.tl && h2 == 0.0 && !stored && aligned16(op.tl);
+    // (measured: pays from n = 8, where the streamed factors dominate the
+    // bytes; at n = 6 the kernel turns FP64-latency bound first)
+    const bool tri = n >= 8 && op.tl && h2 == 0.0 && !stored && aligned16(op.tl);
     if (dinv && h2 != 0.0) return launch_k1_tma<n, true, true, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
     if (h2 != 0.0) return launch_k1_tma<n, false, true, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
     if (dinv)
