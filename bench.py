@@ -65,6 +65,37 @@ def roofline_block(N, E, nodes, k1_ms, k2_ms, it_ms, peak, peak_kind, traffic, k
                           "stored_geometry_bound_gdofs": stored_cap}}
 
 
+def ax_microbench(peak, reps=10):
+    """BASELINE configs[1] / SURVEY C2: the standalone Helmholtz Ax (h1 = h2 = 1)
+    on a 32^3 N=7 deformed box, 1 GPU, u ~ U(-1,1); 1 warm-up + reps, min and
+    median; roofline from 72 algorithmic B/node (u, g1..g6, bm read; w written)."""
+    import torch
+
+    import paper_2109_03592_b200 as sb
+    ctx = sb.Context.box(32, 32, 32, 7, deform=0.05, device=0)
+    g = torch.Generator(device="cuda:0").manual_seed(1)
+    u = torch.rand(ctx.nodes, dtype=torch.float64, device="cuda:0", generator=g) * 2 - 1
+    w = torch.empty_like(u)
+    co = sb.HelmholtzCoeffs(1.0, 1.0)
+    sb.axhelm(u, co, ctx, out=w)
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        sb.axhelm(u, co, ctx, out=w)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    nodes = ctx.nodes
+    ctx.close()
+    tmin, tmed = min(ts), statistics.median(ts)
+    gbs = 72 * nodes / (tmin * 1e-3) / 1e9
+    return {"config": "Helmholtz Ax h1=h2=1, 32^3 N=7 deformed box, 1 GPU (BASELINE configs[1])",
+            "ms_min": tmin, "ms_median": tmed, "gdofs": nodes / (tmin * 1e-3) / 1e9,
+            "algorithmic_bytes_per_node": 72, "achieved_gbs": gbs, "peak": peak,
+            "frac": gbs / peak}
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -79,7 +110,7 @@ class ClockSampler:
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_power_cap,power.draw,power.limit")
 
     def __init__(self, index=0):
         self.index = index
@@ -116,9 +147,20 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4)
                           if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        def num(col):
+            v = []
+            for s in self.samples:
+                try:
+                    v.append(float(s[col]))
+                except (IndexError, ValueError):
+                    pass
+            return v
+        pw, pl = num(6), num(7)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+                "samples": len(self.samples),
+                "power_w": statistics.median(pw) if pw else None,
+                "power_limit_w": max(pl) if pl else None}
 
 
 def parse():
@@ -303,6 +345,7 @@ def run_ours(args):
                                        peak_kind, traffic,
                                        "ax_tma_kernel (K1: p/x update + axhelm + p'Ap)"),
             "clocks": clk.summary()}
+    line["ax_microbench"] = ax_microbench(peak)
     if not args.no_cpu_baseline:
         cex, cey, cez = args.cpu_sample
         times, backend, cores, cnodes = cpu_reference_run(cex, cey, cez, N, args.deform,

@@ -1068,7 +1068,7 @@ int num_sms(int dev) {
 
 // consumer groups of the TRI kernel, bounded by the register budget
 // (65536 / threads): the metric's per-column constants and temporaries
-constexpr int tri_max_groups(int n) { return n <= 8 ? 5 : (n <= 12 ? 2 : 1); }
+constexpr int tri_max_groups(int n) { return n <= 8 ? 4 : (n <= 12 ? 2 : 1); }
 
 // TRI: the metric is formed at each node from the element's trilinear map
 // (op.tl) instead of streaming the 6 stored factors -- 48 fewer bytes per

@@ -7,8 +7,10 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "ax_core.cuh"
+#include "ax_tma.cuh"
 #include "kernels.cuh"
 #include "sbx_internal.h"
 
@@ -103,10 +105,80 @@ __global__ void ax_generic_kernel(const double* __restrict__ u, const double* __
   }
 }
 
+// Standalone FAST axhelm on the persistent TMA pipeline (ax_tma.cuh): stages
+// the packed G, u [, bm] per element; w = h1*DᵀGDu (+ h2*bm*u).  64 / 72
+// algorithmic B/node (Poisson / Helmholtz).
+template <bool HAS_BM>
+struct AxPol {
+  static constexpr int NV = HAS_BM ? 2 : 1;
+  struct Args {
+    const double* u;
+    const double* bm;
+    double* w;
+    double h2;
+  };
+  __device__ static bool init(Args&) { return true; }
+  __device__ static int element_sends(const Args&, int64_t, int) { return 0; }
+  __device__ static void element_done(const Args&, int, int64_t, int, int, int, int, int) {}
+  __device__ static const double* vec(const Args& a, int q) { return q == 0 ? a.u : a.bm; }
+  __device__ static void pro(const Args& a, const double (&v)[NV], int64_t, double& u,
+                             double& hb) {
+    u = v[0];
+    hb = HAS_BM ? a.h2 * v[NV - 1] : 0.0;
+  }
+  __device__ static void epi(const Args& a, double acc, double u, double hb, int64_t idx,
+                             double&) {
+    a.w[idx] = HAS_BM ? fma(hb, u, acc) : acc;
+  }
+  __device__ static void finish(const Args&, double, double*, double*, bool*) {}
+};
+
+template <int n, bool HAS_BM>
+cudaError_t launch_ax_tma(const OpDev& op, const double* u, double* w, double h1, double h2,
+                          double tsign, cudaStream_t s) {
+  using Pol = AxPol<HAS_BM>;
+  using Ch = TmaChoice<n, Pol::NV>;
+  if constexpr (!Ch::ok) {
+    return cudaErrorNotSupported;
+  } else {
+    using L = TmaLayout<n, Pol::NV, Ch::GROUPS, Ch::S>;
+    auto kern = ax_tma_kernel<n, Pol, Ch::GROUPS, Ch::S>;
+    static bool attr_set[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!attr_set[dev & 63]) {
+      cudaError_t err =
+          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::smem);
+      if (err != cudaSuccess) return err;
+      attr_set[dev & 63] = true;
+    }
+    static int sms[64] = {};
+    if (!sms[dev & 63]) cudaDeviceGetAttribute(&sms[dev & 63], cudaDevAttrMultiProcessorCount, dev);
+    DParam<n> Dp;
+    for (int q = 0; q < n * n; ++q) Dp.d[q] = op.Dh[q];
+    QParam<n> Qp{};
+    typename Pol::Args a{u, op.bm, w, h2};
+    const int64_t NG = (op.E + TmaGeom<n>::EPG - 1) / TmaGeom<n>::EPG;
+    int64_t grid = sms[dev & 63] > 0 ? sms[dev & 63] : 148;
+    if (grid > NG) grid = NG;
+    kern<<<(unsigned)grid, L::threads, L::smem, s>>>(a, op.G, op.E, h1, tsign, Dp, nullptr, Qp);
+    return cudaGetLastError();
+  }
+}
+
+inline bool al16(const void* p) { return p == nullptr || ((uintptr_t)p & 15) == 0; }
+
 template <int n, bool EXACT>
 cudaError_t launch_ax_t(const OpDev& op, const double* u, double* w, double h1, double h2,
                         double tsign, cudaStream_t s) {
   using C = AxCfg<n>;
+  static const bool no_tma = std::getenv("SBX_NO_TMA") != nullptr;
+  if (!EXACT && !no_tma && n % 2 == 0 && al16(u) && al16(w) && al16(op.G) &&
+      (h2 == 0.0 || al16(op.bm))) {
+    const cudaError_t e = h2 != 0.0 ? launch_ax_tma<n, true>(op, u, w, h1, h2, tsign, s)
+                                    : launch_ax_tma<n, false>(op, u, w, h1, h2, tsign, s);
+    if (e != cudaErrorNotSupported) return e;
+  }
   static bool attr_set[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
