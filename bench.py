@@ -34,6 +34,11 @@ METRIC = "CG GDOF/s (N=7, FP64, Poisson PCG+Jacobi, deformed box)"
 UNIT = "GDOF/s"
 
 
+def unique_fraction(ex, ey, ez, N):
+    """unique / local DOF of a non-periodic box (SURVEY §8(d) DOF convention)."""
+    return (ex * N + 1) * (ey * N + 1) * (ez * N + 1) / (ex * ey * ez * (N + 1) ** 3)
+
+
 def k1_geometry(N):
     """Which K1 variant the fused CG runs (mirrors launch_k1 in cg.cu): box
     contexts with an even node count 8 <= n = N+1 <= 16 and h2 = 0 form the metric
@@ -177,6 +182,7 @@ def parse():
                     help="mesh of the bounded CPU-baseline sample")
     ap.add_argument("--cpu-iters", type=int, default=30)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ax-microbench", action="store_true")
     return ap.parse_args()
 
 
@@ -345,7 +351,9 @@ def run_ours(args):
                                        peak_kind, traffic,
                                        "ax_tma_kernel (K1: p/x update + axhelm + p'Ap)"),
             "clocks": clk.summary()}
-    line["ax_microbench"] = ax_microbench(peak)
+    line["unique_dof_gdofs"] = value * unique_fraction(ex, ey, ez, N)
+    if not args.no_ax_microbench:
+        line["ax_microbench"] = ax_microbench(peak)
     if not args.no_cpu_baseline:
         cex, cey, cez = args.cpu_sample
         times, backend, cores, cnodes = cpu_reference_run(cex, cey, cez, N, args.deform,
@@ -461,7 +469,8 @@ def run_ours_dist(args):
                                            ms / iters, peak, peak_kind, None,
                                            "ax_tma_kernel (K1, rank 0); k2_ms = halo "
                                            "assembly + K2 + scalar exchange"),
-                "clocks": clocks}
+                "clocks": clocks,
+                "unique_dof_gdofs": value * unique_fraction(ex, ey, ez, N)}
         print(json.dumps(line), flush=True)
     ctx.close()
     dist.barrier()

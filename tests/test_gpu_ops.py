@@ -49,6 +49,8 @@ def test_axhelm_exact_bitwise_and_fast_tol(cuda, case):
     flip = sb.axhelm(u, sb.HelmholtzCoeffs(1.0, 0.0), ctx, exact=True, flip=True)
     assert np.array_equal(flip, P.axhelm(u, 1.0, 0.0, flip=True))
     assert rel_l2(flip, P.axhelm(u, 1.0, 0.0)) > 1e-3
+    fflip = sb.axhelm(u, sb.HelmholtzCoeffs(1.0, 0.0), ctx, flip=True)
+    assert rel_l2(fflip, flip) <= AX_TOL
 
 
 @pytest.mark.parametrize("case", CASES[:10], ids=lambda c: f"N{c[3]}")
