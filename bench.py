@@ -237,8 +237,12 @@ def run_reference_arm(args):
             "ms_per_iteration": t * 1e3 / iters, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": "Poisson PCG, Jacobi, deformed box (a=0.05)",
-                       "elements": [ex, ey, ez], "degree": N, "iterations_per_step": iters},
+            "config": {"workload": "Poisson PCG, Jacobi, deformed box (a=0.05), zero guess",
+                       "elements": list(args.elements), "degree": N,
+                       "iterations_per_step": args.iters,
+                       "parallelism": f"reference CPU pcg, {cores} host threads",
+                       "timed_sample": {"elements": [ex, ey, ez],
+                                        "iterations_per_step": iters}},
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores,
                              "kind": "reference" if backend == "ref" else "port",
                              "sample": sample},

@@ -109,12 +109,10 @@ struct CgK1Pol {
     if (a.dd && a.dd->debug_nosend) a.esend_off = nullptr;  // timing experiments only
     return true;
   }
-  // number of interface sends of a step's element(s): read by the producer
-  // lane one step ahead and handed to the consumers through the slot metadata
-  __device__ static int element_sends(const Args& a, int64_t e0, int cnt) {
-    if (!a.esend_off) return 0;
-    return __ldg(a.esend_off + e0 + cnt) - __ldg(a.esend_off + e0);
-  }
+  // per-element send offsets (CSR): the producer lane prefetches
+  // esend_off[e0], esend_off[e0 + cnt] a few steps ahead and hands the step's
+  // send count to the consumers through the slot metadata
+  __device__ static const int32_t* send_index(const Args& a) { return a.esend_off; }
   // after the element(s) of a step are written: put their interface values in
   // the send buffer (group-uniform; no-op on a single GPU)
   __device__ static void element_done(const Args& a, int nsend, int64_t e0, int cnt, int n3,
@@ -576,6 +574,23 @@ __global__ void __launch_bounds__(AxCfg<n>::threads)
 // thread with per-thread async copies (cp.async, 8 bytes, zero-filled when
 // absent) into a double-buffered staging area ONE group-step AHEAD, so the L2
 // latency of the gathers overlaps the previous step's arithmetic.
+// Thread geometry of K2: one thread per (i, j) column, EPG elements per group
+// step.  The group width is the smallest multiple of 32 (<= 192) that leaves at
+// most 1/8 of the lanes idle, else the plain round-up (n = 6: 160 threads for
+// 4 elements instead of 64 threads with 28 idle).
+template <int n>
+struct K2Geom {
+  static constexpr int nn = n * n;
+  static constexpr int n3 = n * n * n;
+  static constexpr int pick_tg() {
+    for (int tg = ((nn + 31) / 32) * 32; tg <= 192; tg += 32)
+      if (8 * (tg - (tg / nn) * nn) <= tg) return tg;
+    return ((nn + 31) / 32) * 32;
+  }
+  static constexpr int TG = pick_tg();
+  static constexpr int EPG = TG / nn;
+};
+
 template <int n>
 struct K2Stage {
   static constexpr int N = n - 1;
@@ -595,7 +610,7 @@ struct K2Stage {
 
 template <int n, int GROUPS, int SPG>
 struct K2Layout {
-  using T = TmaGeom<n>;
+  using T = K2Geom<n>;
   static constexpr int V_D = ((T::EPG * T::n3 + 1) / 2) * 2 + 2;
   static constexpr int SLOT_D = 3 * V_D;
   static constexpr int S = GROUPS * SPG;
@@ -609,7 +624,7 @@ struct K2Layout {
 
 template <int n>
 struct K2Choice {
-  using T = TmaGeom<n>;
+  using T = K2Geom<n>;
   using L1 = K2Layout<n, 1, 1>;
   static constexpr size_t BUDGET = 225 * 1024 - 512;
   static constexpr size_t slot_bytes = sizeof(double) * L1::SLOT_D + 16;
@@ -636,19 +651,6 @@ struct K2Choice {
 // -3 the node is not on that face (no partner)
 __device__ __forceinline__ bool nb_act(int c) { return c >= 0 || c == -2; }
 
-// 8-byte asynchronous global -> shared copy; zero-filled when !valid
-__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src),
-               "r"(valid ? 8 : 0)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-template <int K>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(K) : "memory");
-}
 
 // A column's view of its element's neighbourhood (from the slot metadata).
 struct ColNb {
@@ -689,7 +691,7 @@ __global__ void __launch_bounds__(K2Layout<n, GROUPS, SPG>::threads, 1)
                          CgScalars* __restrict__ sc, double* __restrict__ partials,
                          double* __restrict__ hist, int64_t hist_cap,
                          cudaGraphConditionalHandle cond, int use_cond) {
-  using T = TmaGeom<n>;
+  using T = K2Geom<n>;
   using L = K2Layout<n, GROUPS, SPG>;
   using St = K2Stage<n>;
   constexpr int S = L::S;
@@ -1169,7 +1171,7 @@ cudaError_t launch_k2(const OpDev& op, const double* w, double* r, const double*
       if (err != cudaSuccess) return err;
       attr_set[op.table][dev & 63] = true;
     }
-    const int64_t NG = (op.E + TmaGeom<n>::EPG - 1) / TmaGeom<n>::EPG;
+    const int64_t NG = (op.E + K2Geom<n>::EPG - 1) / K2Geom<n>::EPG;
     int64_t grid = num_sms(dev);
     if (grid > NG) grid = NG;
     static const int nogather = std::getenv("SBX_K2_NOGATHER") ? 1 : 0;
