@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsbx.so")
+# SBX_LIB: an alternative build of the same library (A/B kernel experiments)
+LIB_PATH = os.environ.get("SBX_LIB") or os.path.join(HERE, "libsbx.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
