@@ -633,6 +633,25 @@ void sbx_ctx_destroy(sbx_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->dd.trace) {
+    // SBX_TRACE=<prefix>: per-iteration timeline of this rank, one line per
+    // iteration: it K1start K1end ifaceStart ifaceWaited K2start K2xchg K2xchgDone (ns)
+    std::vector<unsigned long long> h((size_t)kTraceIters * 8);
+    if (cudaMemcpy(h.data(), c->dd.trace, h.size() * 8, cudaMemcpyDeviceToHost) == cudaSuccess) {
+      const std::string path = std::string(std::getenv("SBX_TRACE") ? std::getenv("SBX_TRACE")
+                                                                     : "sbx_trace") +
+                               ".rank" + std::to_string(c->rank);
+      if (FILE* f = std::fopen(path.c_str(), "w")) {
+        for (int it = 0; it < kTraceIters; ++it) {
+          if (!h[(size_t)it * 8]) continue;
+          std::fprintf(f, "%d", it);
+          for (int q = 0; q < 7; ++q) std::fprintf(f, " %llu", h[(size_t)it * 8 + q]);
+          std::fprintf(f, "\n");
+        }
+        std::fclose(f);
+      }
+    }
+  }
   c->cg.reset();
   for (void* p : c->peer_windows) cudaIpcCloseMemHandle(p);
   if (c->window) cudaFree(c->window);
@@ -1176,6 +1195,12 @@ sbx_status sbx_ctx_dist_connect(sbx_ctx* c, const uint8_t* blobs) {
   // device copy of the exchange state for the fused kernels (K1 epilogue
   // sends, K2 scalar step)
   D.debug_nosend = std::getenv("SBX_DEBUG_NOSEND") ? 1 : 0;
+  if (std::getenv("SBX_TRACE")) {
+    void* tp = nullptr;
+    SBX_TRY(dalloc(c, &tp, sizeof(unsigned long long) * kTraceIters * 8));
+    SBX_CUDA(cudaMemset(tp, 0, sizeof(unsigned long long) * kTraceIters * 8));
+    D.trace = static_cast<unsigned long long*>(tp);
+  }
   void* p = nullptr;
   SBX_TRY(dalloc(c, &p, sizeof(DistDev)));
   SBX_CUDA(cudaMemcpy(p, &c->dd, sizeof(DistDev), cudaMemcpyHostToDevice));

@@ -107,6 +107,7 @@ struct CgK1Pol {
     a.par = a.dd ? (int)((*(const volatile unsigned long long*)a.dd->seq + 1) & 1) : 0;
     a.esend_off = a.dd ? a.dd->esend_off : nullptr;
     if (a.dd && a.dd->debug_nosend) a.esend_off = nullptr;  // timing experiments only
+    if (blockIdx.x == 0 && threadIdx.x == 0) trace_stamp(a.dd, a.sc->it, 0);
     return true;
   }
   // per-element send offsets (CSR): the producer lane prefetches
@@ -160,6 +161,7 @@ __device__ void CgK1Pol<HAS_DINV, HAS_BM>::finish(const Args& a, double red, dou
   if (threadIdx.x == 0 && a.dd) {
     sc->counter[0] = 0;
     sc->pq_loc = tot;  // summed over ranks by dist_iface_kernel
+    trace_stamp(a.dd, sc->it, 1);
     // every CTA fenced its interface stores before its ticket: release the
     // halo and this rank's p'Ap to all ranks
     dist_release_phase0(*a.dd, tot);
@@ -705,6 +707,7 @@ __global__ void __launch_bounds__(K2Layout<n, GROUPS, SPG>::threads, 1)
     return;
   }
   const double alpha = sc->alpha;
+  if (TABLE && blockIdx.x == 0 && threadIdx.x == 0) trace_stamp(dd, sc->it, 4);
   uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
   uint64_t* empty = full + S;
   int32_t* meta = reinterpret_cast<int32_t*>(smraw + L::BAR_BYTES);  // [GROUPS][2][EPG][32]
@@ -1070,7 +1073,10 @@ int num_sms(int dev) {
 
 // consumer groups of the TRI kernel, bounded by the register budget
 // (65536 / threads): the metric's per-column constants and temporaries
-constexpr int tri_max_groups(int n) { return n <= 8 ? 4 : (n <= 12 ? 2 : 1); }
+#ifndef SBX_TRI_G8
+#define SBX_TRI_G8 4
+#endif
+constexpr int tri_max_groups(int n) { return n <= 8 ? SBX_TRI_G8 : (n <= 12 ? 2 : 1); }
 
 // TRI: the metric is formed at each node from the element's trilinear map
 // (op.tl) instead of streaming the 6 stored factors -- 48 fewer bytes per
@@ -1295,7 +1301,9 @@ cudaError_t dist_iteration_tail(const OpDev& op, const DistDev& D, double* w, do
   // K1 (already launched) put the halo on the wire from its epilogue and
   // released phase 0; here: wait + alpha + interface groups, then K2 whose
   // last CTA exchanges r'z / r'r and takes the scalar step.
-  dist_iface_kernel<<<blocks_for(D.n_if, 256, 592), 256, 0, s>>>(D, 0, 0, w, 1, sc);
+  // one thread per interface group: every group's chain of dependent loads
+  // (offsets -> codes -> local / NVLink copies) runs concurrently
+  dist_iface_kernel<<<blocks_for(D.n_if, 128, 16384), 128, 0, s>>>(D, 0, 0, w, 1, sc);
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return err;
   return k2(op, w, r, dinv, sc, partials, hist, hist_cap, cond, use_cond, s);

@@ -48,6 +48,11 @@ __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned lon
   return *reinterpret_cast<const volatile unsigned long long*>(p);
 }
 
+// SBX_TRACE stamp: slot c of iteration it (one thread calls it)
+__device__ __forceinline__ void trace_stamp(const DistDev* D, int it, int c) {
+  if (D && D->trace) D->trace[(it % kTraceIters) * 8 + c] = globaltimer();
+}
+
 // Wait until every other rank released `phase` with sequence >= expected.
 __device__ bool dist_wait_all(const DistDev& D, int phase, unsigned long long expected) {
   const unsigned long long t0 = globaltimer();
@@ -110,8 +115,10 @@ __global__ void dist_iface_kernel(DistDev D, int phase, int slot, double* __rest
   __shared__ bool ok;
   if (sc && sc->done) return;
   if (threadIdx.x == 0) {
+    if (sc && blockIdx.x == 0) trace_stamp(&D, sc->it, 2);
     ok = dist_wait_all(D, phase, ld_volatile_u64(D.seq + phase));
     if (!ok) *D.status = 1;
+    if (sc && blockIdx.x == 0) trace_stamp(&D, sc->it, 3);
   }
   __syncthreads();
   if (!ok) {
@@ -197,6 +204,7 @@ __device__ void dist_scalar_step(const DistDev& D, CgScalars* __restrict__ sc, d
   const int phase = 1;
   const unsigned long long s = ld_volatile_u64(D.seq + phase);
   const double mine[2] = {rz_loc, rr_loc};
+  trace_stamp(&D, sc->it, 5);
   for (int q = 0; q < D.nranks; ++q)
     for (int c = 0; c < 2; ++c)
       D.pmbox[q][mbox_index(phase, (int)((s + 1) & 1), D.rank, c)] = mine[c];
@@ -210,6 +218,7 @@ __device__ void dist_scalar_step(const DistDev& D, CgScalars* __restrict__ sc, d
     if (use_cond) cudaGraphSetConditional(cond, 0);
     return;
   }
+  trace_stamp(&D, sc->it, 6);
   const double rz_new = mbox_sum(D, phase, (int)((s + 1) & 1), 0);
   const double rr_new = mbox_sum(D, phase, (int)((s + 1) & 1), 1);
   const double rnorm = sqrt(rr_new);

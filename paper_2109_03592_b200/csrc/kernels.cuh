@@ -121,7 +121,10 @@ struct DistDev {
   unsigned int* counter = nullptr;    // device [4]
   int* status = nullptr;              // device: 1 on exchange timeout
   int debug_nosend = 0;               // SBX_DEBUG_NOSEND: skip halo sends (timing only)
+  // SBX_TRACE: per-iteration %globaltimer stamps [kTraceIters][8] (diagnostics)
+  unsigned long long* trace = nullptr;
 };
+constexpr int kTraceIters = 4096;
 
 // distributed gather-scatter of a local field (halo exchange over the peer
 // windows, interface groups summed in canonical order, then the local

@@ -46,10 +46,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
-// Producer-side wait: back off between probes so a spinning producer lane
-// does not take issue slots from the consumer warps of its SM sub-partition.
+// Producer-side wait: the thread is suspended in hardware until the phase
+// completes (or the hint, in ns, expires), so a waiting producer lane takes no
+// issue slots from the consumer warps of its SM sub-partition.
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
-  while (!mbar_try_wait(bar, parity)) __nanosleep(64);
+  while (!mbar_try_wait_sleep(bar, parity)) {
+  }
 }
 
 // 1-D bulk copy global -> shared (TMA engine), completion counted on bar.

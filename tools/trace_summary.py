@@ -1,0 +1,39 @@
+"""Median per-iteration timeline of a multi-GPU solve traced with
+SBX_TRACE=<prefix> (one file per rank: <prefix>.rank<r>).
+
+    python tools/trace_summary.py gpurun_out/trace
+"""
+import glob
+import statistics
+import sys
+
+SEG = [("K1 (CTA0 start -> last CTA)", 0, 1), ("K1 end -> iface start", 1, 2),
+       ("iface: wait for peers", 2, 3), ("iface assembly + K2 launch", 3, 4),
+       ("K2 body (-> last CTA)", 4, 5), ("r'z/r'r exchange", 5, 6),
+       ("exchange -> next K1 start", 6, 7)]
+
+
+def main(prefix):
+    for path in sorted(glob.glob(prefix + ".rank*")):
+        rows = [list(map(int, l.split())) for l in open(path)]
+        rows.sort()
+        its = {r[0]: r[1:] for r in rows}
+        acc = {name: [] for name, _, _ in SEG}
+        tot = []
+        for it, t in its.items():
+            if it < 3 or it + 1 not in its:
+                continue
+            nxt = its[it + 1][0]
+            t = t + [nxt]
+            if min(t) == 0:
+                continue
+            for name, a, b in SEG:
+                acc[name].append((t[b] - t[a]) / 1e3)
+            tot.append((nxt - t[0]) / 1e3)
+        print(f"{path}: {len(tot)} iterations, median {statistics.median(tot):.1f} us/iteration")
+        for name, _, _ in SEG:
+            print(f"  {name:32s} {statistics.median(acc[name]):8.1f} us")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])
