@@ -952,8 +952,8 @@ namespace {
 
 struct DistBlob {
   cudaIpcMemHandle_t handle;
-  int64_t send_total;                 // size of one send-buffer parity region
-  int64_t send_base_for_dst[kMaxRanks];  // my block destined to rank q (-1: none)
+  int64_t recv_total;                 // size of one receive-buffer parity region
+  int64_t recv_base_for_src[kMaxRanks];  // where rank q's block lands in it (-1: none)
 };
 
 sbx_status upload_dist(sbx_ctx* c, const DistPlan& P, const sbx_box_desc* d) {
@@ -1075,16 +1075,16 @@ sbx_status upload_dist(sbx_ctx* c, const DistPlan& P, const sbx_box_desc* d) {
   // peer window (exported over CUDA IPC; own allocation, not via dalloc's list
   // so it is freed after the peers close their mappings)
   const size_t wbytes =
-      kWinRecv + sizeof(double) * (size_t)std::max<int64_t>(4 * D.send_total, 2);
+      kWinRecv + sizeof(double) * (size_t)std::max<int64_t>(4 * D.recv_total, 2);
   SBX_CUDA(cudaMalloc(&c->window, wbytes));
   SBX_CUDA(cudaMemsetAsync(c->window, 0, wbytes, c->stream));
   char* wb = static_cast<char*>(c->window);
   D.flags = reinterpret_cast<unsigned long long*>(wb + kWinFlags);
   D.mbox = reinterpret_cast<double*>(wb + kWinMbox);
-  D.sendb = reinterpret_cast<double*>(wb + kWinRecv);
-  // per destination rank: offset of its block in my send buffer (-1: none)
+  D.recvb = reinterpret_cast<double*>(wb + kWinRecv);
+  // per source rank: offset of its block in my receive buffer (-1: none)
   c->recv_base_for_src.assign(kMaxRanks, -1);
-  for (int qi = 0; qi < D.nnbr; ++qi) c->recv_base_for_src[P.nbr[qi]] = D.send_off[qi];
+  for (int qi = 0; qi < D.nnbr; ++qi) c->recv_base_for_src[P.nbr[qi]] = D.recv_base[qi];
   SBX_TRY(ensure_partials(c, std::max<int64_t>(EL, 4096)));
   c->cg.reset(new CgEngine());
   SBX_CUDA(cudaStreamSynchronize(c->stream));
@@ -1150,8 +1150,8 @@ sbx_status sbx_ctx_dist_blob(sbx_ctx* c, uint8_t* blob) {
   DistBlob b;
   std::memset(&b, 0, sizeof(b));
   SBX_CUDA(cudaIpcGetMemHandle(&b.handle, c->window));
-  b.send_total = c->dd.send_total;
-  for (int q = 0; q < kMaxRanks; ++q) b.send_base_for_dst[q] = c->recv_base_for_src[q];
+  b.recv_total = c->dd.recv_total;
+  for (int q = 0; q < kMaxRanks; ++q) b.recv_base_for_src[q] = c->recv_base_for_src[q];
   std::memcpy(blob, &b, sizeof(b));
   return SBX_OK;
 }
@@ -1178,15 +1178,15 @@ sbx_status sbx_ctx_dist_connect(sbx_ctx* c, const uint8_t* blobs) {
     }
     D.pflags[q] = reinterpret_cast<unsigned long long*>(base + kWinFlags);
     D.pmbox[q] = reinterpret_cast<double*>(base + kWinMbox);
-    D.psend[q] = reinterpret_cast<double*>(base + kWinRecv);
-    D.psend_total[q] = b.send_total;
-    D.pbase_from[q] = b.send_base_for_dst[c->rank];
+    D.precv[q] = reinterpret_cast<double*>(base + kWinRecv);
+    D.precv_total[q] = b.recv_total;
+    D.pbase_for_me[q] = b.recv_base_for_src[c->rank];
     if (q != c->rank) {
       // a neighbour must hold a send block for me, and I for it
       bool i_send = false;
       for (int qi = 0; qi < D.nnbr; ++qi)
         if (D.nbr[qi] == q) i_send = true;
-      if (i_send != (b.send_base_for_dst[c->rank] >= 0)) {
+      if (i_send != (b.recv_base_for_src[c->rank] >= 0)) {
         set_error("sbx_ctx_dist_connect: inconsistent exchange plans between ranks");
         return SBX_E_COMM;
       }

@@ -98,6 +98,7 @@ struct CgK1Pol {
     int first;
     int par;  // send-buffer parity of this iteration's halo (phase 0)
     const int32_t* esend_off;
+    int stored;  // this thread pushed halo values (fence before the ticket)
   };
   __device__ static bool init(Args& a) {
     if (a.sc->done) return false;
@@ -116,11 +117,11 @@ struct CgK1Pol {
   __device__ static const int32_t* send_index(const Args& a) { return a.esend_off; }
   // after the element(s) of a step are written: put their interface values in
   // the send buffer (group-uniform; no-op on a single GPU)
-  __device__ static void element_done(const Args& a, int nsend, int64_t e0, int cnt, int n3,
-                                      int lt, int tg, int bar) {
+  __device__ static void element_done(Args& a, int nsend, int64_t e0, int cnt, int n3, int lt,
+                                      int tg, int bar) {
     if (nsend == 0) return;
     named_bar_sync(bar, tg);  // w of the step visible to the whole group
-    dist_send_elements(a.dd, a.par, a.w, e0, cnt, n3, lt, tg);
+    if (dist_send_elements(a.dd, a.par, a.w, e0, cnt, n3, lt, tg)) a.stored = 1;
   }
   __device__ static const double* vec(const Args& a, int q) {
     return q == 0 ? a.r : q == 1 ? a.p : q == 2 ? a.x : (HAS_DINV && q == QD) ? a.dinv : a.bm;
@@ -150,9 +151,10 @@ struct CgK1Pol {
 template <bool HAS_DINV, bool HAS_BM>
 __device__ void CgK1Pol<HAS_DINV, HAS_BM>::finish(const Args& a, double red, double* partials,
                                                   double* sh, bool* flag) {
-  // (dist: the CTA's send-buffer stores are published by last_block's
-  // barrier + GPU-scope fence before the ticket, then released at system
-  // scope by dist_release_phase0)
+  // (dist: a thread that pushed halo values over NVLink fences them at
+  // system scope once, here, before the CTA's ticket; the last CTA then
+  // releases them with dist_release_phase0)
+  if (a.stored) __threadfence_system();
   const double v = cta_sum(red, sh);
   if (threadIdx.x == 0) partials[blockIdx.x] = v;
   CgScalars* sc = a.sc;
@@ -1106,7 +1108,7 @@ cudaError_t launch_k1_tma(const OpDev& op, const double* r, const double* dinv, 
       Qp.x[q] = op.Xh[q];
       Qp.w[q] = op.Wh[q];
     }
-    typename Pol::Args a{r, dinv, p, x, w, op.bm, h2, sc, op.dd, 0.0, 0.0, 0, 0, nullptr};
+    typename Pol::Args a{r, dinv, p, x, w, op.bm, h2, sc, op.dd, 0.0, 0.0, 0, 0, nullptr, 0};
     const int64_t NG = (op.E + TmaGeom<n>::EPG - 1) / TmaGeom<n>::EPG;
     int64_t grid = num_sms(dev);
     if (grid > NG) grid = NG;

@@ -1,9 +1,10 @@
 // Peer-window exchange kernels for the distributed PCG (included by cg.cu).
 //
-// A sender writes raw copy values into its OWN send buffer, publishes them at
-// GPU scope and releases a per-(phase, source) sequence flag in every peer's
-// window; the receiver acquires the flags of all ranks, then pulls the blocks
-// destined to it over NVLink (IPC-mapped peer pointers).  Scalars travel in
+// A sender stores raw copy values straight into its neighbours' receive
+// buffers over NVLink (IPC-mapped peer pointers), fences them at system scope
+// once per storing thread, and releases a per-(phase, source) sequence flag in
+// every peer's window; the receiver acquires the flags, then reads its own
+// receive buffer.  Scalars travel in
 // per-source mailboxes and are summed in rank order, so every rank computes
 // bit-identical CG scalars.  Waits are bounded (kSpinTimeoutNs) and report a
 // communication error instead of hanging.
@@ -76,11 +77,18 @@ __global__ void dist_put_kernel(DistDev D, int phase, int slot, const double* __
   const unsigned long long s = ld_volatile_u64(D.seq + phase);
   const int64_t par = (int64_t)((s + 1) & 1);
   const int64_t total = D.send_off[D.nnbr];
-  // pack into this rank's own send buffer (the peers pull it)
-  double* sb = D.sendb + (slot * 2 + par) * D.send_total;
+  // push into the neighbours' receive buffers over NVLink
+  bool stored = false;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x)
-    sb[i] = w[D.send_idx[i]];
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int qi = 0;
+    while (i >= D.send_off[qi + 1]) ++qi;
+    const int q = D.nbr[qi];
+    D.precv[q][(slot * 2 + par) * D.precv_total[q] + D.pbase_for_me[q] + (i - D.send_off[qi])] =
+        w[D.send_idx[i]];
+    stored = true;
+  }
+  if (stored) __threadfence_system();  // this thread's remote stores, before the ticket
   dist_fence();
   __syncthreads();
   if (threadIdx.x == 0) last = atomicAdd(D.counter + phase, 1u) == gridDim.x - 1;
@@ -141,11 +149,8 @@ __global__ void dist_iface_kernel(DistDev D, int phase, int slot, double* __rest
   }
   const int64_t par = (int64_t)(ld_volatile_u64(D.seq + phase) & 1);
   // remote copies are pulled from the owners' send buffers over NVLink
-  const double* src[kMaxRanks];
-  for (int qi = 0; qi < D.nnbr; ++qi) {
-    const int q = D.nbr[qi];
-    src[qi] = D.psend[q] + (slot * 2 + par) * D.psend_total[q] + D.pbase_from[q];
-  }
+  // remote copies were pushed into this rank's receive buffer
+  const double* rb = D.recvb + (int64_t)(slot * 2 + par) * D.recv_total;
   const int64_t NL = D.nodes_local;
   for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < D.n_if;
        g += (int64_t)gridDim.x * blockDim.x) {
@@ -155,10 +160,7 @@ __global__ void dist_iface_kernel(DistDev D, int phase, int slot, double* __rest
       const int32_t code = D.if_code[c];
       double v;
       if (code >= NL) {
-        const int64_t rpos = code - NL;
-        int qi = 0;
-        while (rpos >= D.recv_base[qi + 1]) ++qi;
-        v = __ldcv(src[qi] + (rpos - D.recv_base[qi]));
+        v = __ldcv(rb + (code - NL));
       } else {
         v = f[code < 0 ? ~code : code];
       }
@@ -249,21 +251,27 @@ __device__ void dist_scalar_step(const DistDev& D, CgScalars* __restrict__ sc, d
 }
 
 // Sends of one element-step from the Ax epilogue: the group's threads store
-// the interface values of its element(s) into this rank's send buffer
-// (phase 0, neighbour-major blocks pulled by the peers).  Called by every
-// thread of a consumer group; group-uniform control flow.
-__device__ __forceinline__ void dist_send_elements(const DistDev* __restrict__ D, int par,
+// the interface values of its element(s) straight into the neighbours'
+// receive buffers (phase 0, slot 0) over NVLink.  Called by every thread of a
+// consumer group; group-uniform control flow.  Returns whether this thread
+// stored anything.
+__device__ __forceinline__ bool dist_send_elements(const DistDev* __restrict__ D, int par,
                                                    const double* __restrict__ w, int64_t e0,
                                                    int cnt, int n3, int lt, int tg) {
-  // (published by the last-CTA ticket's fence, released by
-  // dist_release_phase0)
-  double* sb = D->sendb + (int64_t)par * D->send_total;  // slot 0 (the CG loop)
+  // (each storing thread fences at system scope once, at the end of K1,
+  // before the last-CTA ticket; released by dist_release_phase0)
+  bool stored = false;
   for (int el = 0; el < cnt; ++el) {
     const int64_t e = e0 + el;
     const int lo = D->esend_off[e], hi = D->esend_off[e + 1];
-    for (int c = lo + lt; c < hi; c += tg)
-      sb[D->send_off[D->esend_q[c]] + D->esend_pos[c]] = w[e * n3 + D->esend_node[c]];
+    for (int c = lo + lt; c < hi; c += tg) {
+      const int q = D->nbr[D->esend_q[c]];
+      D->precv[q][(int64_t)par * D->precv_total[q] + D->pbase_for_me[q] + D->esend_pos[c]] =
+          w[e * n3 + D->esend_node[c]];
+      stored = true;
+    }
   }
+  return stored;
 }
 
 // Release of phase 0 by the last CTA of K1 (one thread): this rank's p'Ap

@@ -75,12 +75,13 @@ struct CgScalars {
 // ---- multi-GPU peer windows ------------------------------------------------
 constexpr int kMaxRanks = 8;
 // Window layout (bytes): flags [4 phases][kMaxRanks] u64 at 0, mailboxes
-// [4 phases][2 parities][kMaxRanks][4] f64 at 256, SEND buffers
-// [2 slots][2 parities][send_total] f64 at 2304.  Phases: 0 halo+p'Ap in the
+// [4 phases][2 parities][kMaxRanks][4] f64 at 256, RECEIVE buffers
+// [2 slots][2 parities][recv_total] f64 at 2304.  Phases: 0 halo+p'Ap in the
 // CG loop, 1 r'z/r'r, 2 standalone gather-scatter halo, 3 setup reductions.
-// The halo is PULLED: a rank writes its interface copy values into its own
-// send buffer (neighbour-major blocks), releases its flag, and the peers read
-// the blocks over NVLink.  Parity = sequence number & 1: a peer can run at most
+// The halo is PUSHED: a sender stores its interface copy values into each
+// neighbour's receive buffer over NVLink as soon as they are computed (the
+// K1 epilogue), fences them at system scope once per thread, and releases its
+// flag; the receiver then reads only local memory.  Parity = sequence number & 1: a peer can run at most
 // one use of a phase ahead (it needs this rank's flag of the previous use), so
 // double buffering makes every access race-free.
 constexpr size_t kWinFlags = 0, kWinMbox = 256, kWinRecv = 2304;
@@ -94,14 +95,14 @@ struct DistDev {
   int64_t nodes_local = 0;
   unsigned long long* flags = nullptr;  // my window
   double* mbox = nullptr;
-  double* sendb = nullptr;              // my send buffer [2 slots][2 par][send_total]
+  double* recvb = nullptr;              // my receive buffer [2 slots][2 par][recv_total]
   int64_t recv_total = 0;
   int64_t send_total = 0;
   unsigned long long* pflags[kMaxRanks] = {};  // peer windows (own rank: mine)
   double* pmbox[kMaxRanks] = {};
-  double* psend[kMaxRanks] = {};
-  int64_t psend_total[kMaxRanks] = {};
-  int64_t pbase_from[kMaxRanks] = {};  // offset of peer q's block destined to me
+  double* precv[kMaxRanks] = {};       // peer q's receive buffer
+  int64_t precv_total[kMaxRanks] = {};
+  int64_t pbase_for_me[kMaxRanks] = {};  // offset of my block in q's receive buffer
   int nnbr = 0;
   int nbr[kMaxRanks] = {};
   int64_t send_off[kMaxRanks + 1] = {};

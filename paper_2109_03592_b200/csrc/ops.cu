@@ -119,7 +119,7 @@ struct AxPol {
   };
   __device__ static bool init(Args&) { return true; }
   __device__ static const int32_t* send_index(const Args&) { return nullptr; }
-  __device__ static void element_done(const Args&, int, int64_t, int, int, int, int, int) {}
+  __device__ static void element_done(Args&, int, int64_t, int, int, int, int, int) {}
   __device__ static const double* vec(const Args& a, int q) { return q == 0 ? a.u : a.bm; }
   __device__ static void pro(const Args& a, const double (&v)[NV], int64_t, double& u,
                              double& hb) {
