@@ -1078,7 +1078,10 @@ int num_sms(int dev) {
 #ifndef SBX_TRI_G8
 #define SBX_TRI_G8 4
 #endif
-constexpr int tri_max_groups(int n) { return n <= 8 ? SBX_TRI_G8 : (n <= 12 ? 2 : 1); }
+#ifndef SBX_TRI_G12
+#define SBX_TRI_G12 2
+#endif
+constexpr int tri_max_groups(int n) { return n <= 8 ? SBX_TRI_G8 : (n <= 12 ? SBX_TRI_G12 : 1); }
 
 // TRI: the metric is formed at each node from the element's trilinear map
 // (op.tl) instead of streaming the 6 stored factors -- 48 fewer bytes per
