@@ -133,7 +133,7 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 8])
 def test_distributed_gs_plan_bitwise(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()

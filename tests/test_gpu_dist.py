@@ -31,3 +31,18 @@ def test_dist_check(cuda, ranks):
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
     assert out.stdout.count("ALL OK") == ranks
+
+
+def test_dist_check_8_ranks_oversubscribed(cuda):
+    """The 8-rank limit (kMaxRanks) with 8 processes on the available GPUs (two
+    or more per device): the exchange plan, mailboxes and flags of every rank
+    pair at the largest supported world size."""
+    if cuda.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=8",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+           os.path.join(ROOT, "tools", "dist_check.py")]
+    env = dict(os.environ, SBX_OVERSUB="1")
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
+    assert out.stdout.count("ALL OK") == 8

@@ -21,8 +21,16 @@ import torch.distributed as dist  # noqa: E402
 
 def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    # SBX_OVERSUB=1: more ranks than GPUs (rank r on GPU r % count; the blob
+    # exchange then runs over gloo, since NCCL refuses two ranks per GPU) --
+    # exercises the 8-rank exchange logic on a 4-GPU box
+    if os.environ.get("SBX_OVERSUB"):
+        local = local % torch.cuda.device_count()
+        torch.cuda.set_device(local)
+        dist.init_process_group("gloo")
+    else:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     rank, world = dist.get_rank(), dist.get_world_size()
     import paper_2109_03592_b200 as sb
     from oracle import oracle as O
