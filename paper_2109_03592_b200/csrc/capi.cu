@@ -1194,7 +1194,6 @@ sbx_status sbx_ctx_dist_connect(sbx_ctx* c, const uint8_t* blobs) {
   }
   // device copy of the exchange state for the fused kernels (K1 epilogue
   // sends, K2 scalar step)
-  D.debug_nosend = std::getenv("SBX_DEBUG_NOSEND") ? 1 : 0;
   if (std::getenv("SBX_TRACE")) {
     void* tp = nullptr;
     SBX_TRY(dalloc(c, &tp, sizeof(unsigned long long) * kTraceIters * 8));

@@ -107,7 +107,6 @@ struct CgK1Pol {
     a.ap = a.sc->alpha_prev;
     a.par = a.dd ? (int)((*(const volatile unsigned long long*)a.dd->seq + 1) & 1) : 0;
     a.esend_off = a.dd ? a.dd->esend_off : nullptr;
-    if (a.dd && a.dd->debug_nosend) a.esend_off = nullptr;  // timing experiments only
     if (blockIdx.x == 0 && threadIdx.x == 0) trace_stamp(a.dd, a.sc->it, 0);
     return true;
   }
@@ -327,7 +326,6 @@ __device__ __forceinline__ void update_tail(double rz, double rr, double alpha, 
 struct BoxP {
   int ex, ey, ez;
   int px, py, pz;
-  int dbg;  // timing experiment only: skip the gathers (wrong result)
 };
 
 // Per-direction sharing state of a node on the structured box: whether the
@@ -365,93 +363,6 @@ __device__ __forceinline__ Dir dir_state(int loc, int N, int c, int count, int p
   return s;
 }
 
-// Flat structured-box update kernel: one node per thread, grid-stride, full
-// occupancy; a shared node's assembled value is re-summed by every copy from
-// the cell lattice in the reference's copy order (z-side outer, y, x inner;
-// smaller element id first), so every copy gets identical bits and no CSR is
-// read.  Own w/r/dinv streams are coalesced; partner copies are L2 hits.
-template <int n>
-__global__ void __launch_bounds__(kUpdThreads)
-    cg_update_flat_kernel(const double* __restrict__ w, double* __restrict__ r,
-                          const double* __restrict__ dinv, int64_t E, BoxP bx,
-                          CgScalars* __restrict__ sc, double* __restrict__ partials,
-                          double* __restrict__ hist, int64_t hist_cap,
-                          cudaGraphConditionalHandle cond, int use_cond) {
-  constexpr int N = n - 1;
-  constexpr int nn = n * n, n3 = n * n * n;
-  __shared__ double red[32];
-  __shared__ bool is_last;
-  if (sc->done) {
-    if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0);
-    return;
-  }
-  const double alpha = sc->alpha;
-  const int64_t exy = (int64_t)bx.ex * bx.ey;
-  const int64_t total = E * n3;
-  double rz = 0.0, rr = 0.0;
-  for (int64_t a = (int64_t)blockIdx.x * kUpdThreads + threadIdx.x; a < total;
-       a += (int64_t)gridDim.x * kUpdThreads) {
-    const uint32_t e = (uint32_t)(a / n3);
-    const int l = (int)(a - (int64_t)e * n3);
-    const int i = l % n, j = (l / n) % n, k = l / nn;
-    const double wo = __ldg(w + a);
-    const double ro = r[a];
-    const double dv = dinv ? __ldg(dinv + a) : 1.0;
-    const bool bnd = i == 0 || i == N || j == 0 || j == N || k == 0 || k == N;
-    double q = wo;
-    int cnt = 0;
-    if (bnd) {
-      const uint32_t cxy = e % (uint32_t)exy;
-      const int cx = (int)(cxy % (uint32_t)bx.ex), cy = (int)(cxy / (uint32_t)bx.ex);
-      const int cz = (int)(e / (uint32_t)exy);
-      const Dir X = dir_state(i, N, cx, bx.ex, bx.px, 1);
-      const Dir Y = dir_state(j, N, cy, bx.ey, bx.py, bx.ex);
-      const Dir Z = dir_state(k, N, cz, bx.ez, bx.pz, exy);
-      cnt = X.act + Y.act + Z.act;
-      if (X.msk || Y.msk || Z.msk) {
-        q = 0.0;
-      } else if (cnt) {
-        double s = 0.0;
-#pragma unroll
-        for (int zs = 0; zs < 2; ++zs) {
-          if (zs == 1 && !Z.act) break;
-          const bool zn = Z.act && ((zs == 0) == Z.nfirst);
-#pragma unroll
-          for (int ys = 0; ys < 2; ++ys) {
-            if (ys == 1 && !Y.act) break;
-            const bool yn = Y.act && ((ys == 0) == Y.nfirst);
-#pragma unroll
-            for (int xs = 0; xs < 2; ++xs) {
-              if (xs == 1 && !X.act) break;
-              const bool xn = X.act && ((xs == 0) == X.nfirst);
-              if (!zn && !yn && !xn) {
-                s += wo;
-              } else {
-                const int64_t ce = (int64_t)e + (xn ? X.d : 0) + (yn ? Y.d : 0) + (zn ? Z.d : 0);
-                const int kk = zn ? N - k : k, jj = yn ? N - j : j, ii = xn ? N - i : i;
-                s += __ldg(w + ce * n3 + (kk * n + jj) * n + ii);
-              }
-            }
-          }
-        }
-        q = s;
-      }
-    }
-    const double wgt = cnt == 0 ? 1.0 : cnt == 1 ? 0.5 : cnt == 2 ? 0.25 : 0.125;
-    const double rv = fma(-alpha, q, ro);
-    r[a] = rv;
-    const double z = rv * dv;
-    rz = fma(rv * z, wgt, rz);
-    rr = fma(rv * rv, wgt, rr);
-  }
-  update_tail(rz, rr, alpha, red, &is_last, sc, partials, hist, hist_cap, cond, use_cond);
-}
-
-// Structured-box update kernel: same work as cg_update_kernel but element-
-// centric (thread per (i,j) column, loop over k, coalesced r/w/dinv streams);
-// a shared node's assembled value is re-summed by every copy from the cell
-// lattice in the reference's copy order (z-side outer, y, x inner; smaller
-// element id first), so all copies get identical bits and no CSR is read.
 template <int n>
 __global__ void __launch_bounds__(AxCfg<n>::threads)
     cg_update_box_kernel(const double* __restrict__ w, double* __restrict__ r,
@@ -480,11 +391,10 @@ __global__ void __launch_bounds__(AxCfg<n>::threads)
     const int ee = (int)e;
     const int cx = ee % bx.ex, cy = (ee / bx.ex) % bx.ey, cz = ee / (bx.ex * bx.ey);
     const int64_t exy = (int64_t)bx.ex * bx.ey;
-    const Dir none{0, false, false, 0};
-    const Dir X = bx.dbg ? none : dir_state(i, N, cx, bx.ex, bx.px, 1);
-    const Dir Y = bx.dbg ? none : dir_state(j, N, cy, bx.ey, bx.py, bx.ex);
-    const Dir Z0 = bx.dbg ? none : dir_state(0, N, cz, bx.ez, bx.pz, exy);
-    const Dir ZN = bx.dbg ? none : dir_state(N, N, cz, bx.ez, bx.pz, exy);
+    const Dir X = dir_state(i, N, cx, bx.ex, bx.px, 1);
+    const Dir Y = dir_state(j, N, cy, bx.ey, bx.py, bx.ex);
+    const Dir Z0 = dir_state(0, N, cz, bx.ez, bx.pz, exy);
+    const Dir ZN = dir_state(N, N, cz, bx.ez, bx.pz, exy);
     const bool mxy = X.msk || Y.msk;
     // column pointers of the own copy and the copies across x, y and x+y
     const double* pw = w + e * C::n3 + ij;
@@ -769,7 +679,6 @@ __global__ void __launch_bounds__(K2Layout<n, GROUPS, SPG>::threads, 1)
       if constexpr (TABLE) {
         return __ldg(nbr27 + ee * 27 + d);
       } else {
-        if (bx.dbg) return -3;  // timing experiment only: no partners
         const int dx = d % 3 - 1, dy = (d / 3) % 3 - 1, dz = d / 9 - 1;
         const uint32_t ue = (uint32_t)ee, uex = (uint32_t)bx.ex, uey = (uint32_t)bx.ey;
         const uint32_t qq = ue / uex;
@@ -1165,9 +1074,8 @@ cudaError_t launch_k2(const OpDev& op, const double* w, double* r, const double*
                       CgScalars* sc, double* partials, double* hist, int64_t hist_cap,
                       cudaGraphConditionalHandle cond, int use_cond, cudaStream_t s) {
   static const bool use_col = std::getenv("SBX_K2_COLUMN") != nullptr;
-  static const bool use_flat = std::getenv("SBX_K2_FLAT") != nullptr;
   static const bool no_tma = std::getenv("SBX_NO_TMA") != nullptr;
-  if (op.box && !use_col && !use_flat && !no_tma && n % 2 == 0 && aligned16(w) &&
+  if (op.box && !use_col && !no_tma && n % 2 == 0 && aligned16(w) &&
       aligned16(r) && aligned16(dinv) && K2Choice<n>::ok) {
     using Ch = K2Choice<n>;
     using L = K2Layout<n, Ch::GROUPS, Ch::SPG>;
@@ -1185,27 +1093,9 @@ cudaError_t launch_k2(const OpDev& op, const double* w, double* r, const double*
     const int64_t NG = (op.E + K2Geom<n>::EPG - 1) / K2Geom<n>::EPG;
     int64_t grid = num_sms(dev);
     if (grid > NG) grid = NG;
-    static const int nogather = std::getenv("SBX_K2_NOGATHER") ? 1 : 0;
-    BoxP bx{op.ex, op.ey, op.ez, op.per[0], op.per[1], op.per[2], nogather};
+    BoxP bx{op.ex, op.ey, op.ez, op.per[0], op.per[1], op.per[2]};
     kern<<<(unsigned)grid, L::threads, L::smem, s>>>(w, r, dinv, op.E, bx, op.nbr27, op.dd, sc,
                                                      partials, hist, hist_cap, cond, use_cond);
-    return cudaGetLastError();
-  }
-  if (op.box && use_flat) {
-    static int per_sm_f[64] = {};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (!per_sm_f[dev & 63]) {
-      int v = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, cg_update_flat_kernel<n>, kUpdThreads, 0);
-      per_sm_f[dev & 63] = v > 0 ? v : 1;
-    }
-    int64_t blocks = (op.nodes + kUpdThreads - 1) / kUpdThreads;
-    const int64_t cap = (int64_t)num_sms(dev) * per_sm_f[dev & 63];
-    if (blocks > cap) blocks = cap;
-    BoxP bx{op.ex, op.ey, op.ez, op.per[0], op.per[1], op.per[2], std::getenv("SBX_K2_NOGATHER") ? 1 : 0};
-    cg_update_flat_kernel<n><<<(unsigned)blocks, kUpdThreads, 0, s>>>(
-        w, r, dinv, op.E, bx, sc, partials, hist, hist_cap, cond, use_cond);
     return cudaGetLastError();
   }
   if (op.box) {
@@ -1221,7 +1111,7 @@ cudaError_t launch_k2(const OpDev& op, const double* w, double* r, const double*
     int64_t blocks = (op.E + C::EPB - 1) / C::EPB;
     const int64_t cap = (int64_t)num_sms(dev) * per_sm[dev & 63];
     if (blocks > cap) blocks = cap;
-    BoxP bx{op.ex, op.ey, op.ez, op.per[0], op.per[1], op.per[2], std::getenv("SBX_K2_NOGATHER") ? 1 : 0};
+    BoxP bx{op.ex, op.ey, op.ez, op.per[0], op.per[1], op.per[2]};
     cg_update_box_kernel<n><<<(unsigned)blocks, C::threads, 0, s>>>(
         w, r, dinv, op.E, bx, sc, partials, hist, hist_cap, cond, use_cond);
     return cudaGetLastError();

@@ -121,7 +121,6 @@ struct DistDev {
   unsigned long long* seq = nullptr;  // device [4]
   unsigned int* counter = nullptr;    // device [4]
   int* status = nullptr;              // device: 1 on exchange timeout
-  int debug_nosend = 0;               // SBX_DEBUG_NOSEND: skip halo sends (timing only)
   // SBX_TRACE: per-iteration %globaltimer stamps [kTraceIters][8] (diagnostics)
   unsigned long long* trace = nullptr;
 };
