@@ -84,6 +84,7 @@ struct CgK1Pol {
   static constexpr int NV = 3 + (HAS_DINV ? 1 : 0) + (HAS_BM ? 1 : 0);
   static constexpr int QD = 3;
   static constexpr int QB = HAS_DINV ? 4 : 3;
+  static constexpr int BMQ = HAS_BM ? QB : -1;
   struct Args {
     const double* r;
     const double* dinv;
@@ -137,6 +138,7 @@ struct CgK1Pol {
     a.p[idx] = u;
     hb = HAS_BM ? a.h2 * v[QB] : 0.0;
   }
+  __device__ static double hb_of(const Args& a, double bm) { return a.h2 * bm; }
   __device__ static void epi(const Args& a, double acc, double u, double hb, int64_t idx,
                              double& red) {
     const double w = HAS_BM ? fma(hb, u, acc) : acc;
@@ -1045,9 +1047,14 @@ cudaError_t launch_k1(const OpDev& op, const double* r, const double* dinv, doub
     static const bool stored = std::getenv("SBX_STORED_GEOMETRY") != nullptr;
     // (measured: pays from n = 8, where the streamed factors dominate the
     // bytes; at n = 6 the kernel turns FP64-latency bound first)
-    const bool tri = n >= 8 && op.tl && h2 == 0.0 && !stored && aligned16(op.tl);
-    if (dinv && h2 != 0.0) return launch_k1_tma<n, true, true, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
-    if (h2 != 0.0) return launch_k1_tma<n, false, true, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
+    // (Helmholtz, h2 != 0: the mass term h2*bm*p still streams bm, 8 B/node)
+    const bool tri = n >= 8 && op.tl && !stored && aligned16(op.tl);
+    if (dinv && h2 != 0.0)
+      return tri ? launch_k1_tma<n, true, true, true>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev)
+                 : launch_k1_tma<n, true, true, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
+    if (h2 != 0.0)
+      return tri ? launch_k1_tma<n, false, true, true>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev)
+                 : launch_k1_tma<n, false, true, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
     if (dinv)
       return tri ? launch_k1_tma<n, true, false, true>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev)
                  : launch_k1_tma<n, true, false, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);

@@ -111,6 +111,7 @@ __global__ void ax_generic_kernel(const double* __restrict__ u, const double* __
 template <bool HAS_BM>
 struct AxPol {
   static constexpr int NV = HAS_BM ? 2 : 1;
+  static constexpr int BMQ = HAS_BM ? 1 : -1;
   struct Args {
     const double* u;
     const double* bm;
@@ -126,6 +127,7 @@ struct AxPol {
     u = v[0];
     hb = HAS_BM ? a.h2 * v[NV - 1] : 0.0;
   }
+  __device__ static double hb_of(const Args& a, double bm) { return a.h2 * bm; }
   __device__ static void epi(const Args& a, double acc, double u, double hb, int64_t idx,
                              double&) {
     a.w[idx] = HAS_BM ? fma(hb, u, acc) : acc;

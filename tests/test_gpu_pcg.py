@@ -129,3 +129,20 @@ def test_pcg_fast_noncontinuous_rhs_falls_back(cuda):
         else:
             r = sb.pcg(op, b, x, sb.KrylovConfig(1e-8, 500), mode="fast")
             assert r.iterations == ref.iterations and np.array_equal(x, ref.x)
+
+
+@pytest.mark.parametrize("N", [5, 7, 9])
+def test_pcg_fast_helmholtz_even_n(cuda, N):
+    """Helmholtz (h1 = 1, h2 = 1) FAST PCG on the TMA path (even n: the
+    trilinear-metric K1 for n >= 8, with h2*bm streamed), against the oracle:
+    same iteration count, solution within 1e-10."""
+    ctx = sb.Context.box(3, 3, 2, N, deform=0.05)
+    P = O.Problem(3, 3, 2, N, corners=O.box_corners(3, 3, 2, deform=0.05))
+    b = P.rhs_random_continuous(21)
+    ref = P.pcg(b, 1.0, 1.0, "jacobi", 1e-10, 2000)
+    op = sb.HelmholtzOperator(ctx, sb.HelmholtzCoeffs(1.0, 1.0))
+    x = np.zeros_like(b)
+    r = sb.pcg(op, b, x, sb.KrylovConfig(1e-10, 2000), mode="fast")
+    assert r.converged and r.iterations == ref.iterations
+    err = np.linalg.norm(x - ref.x) / np.linalg.norm(ref.x)
+    assert err <= FINAL_TOL
