@@ -41,7 +41,7 @@ def unique_fraction(ex, ey, ez, N):
 
 def k1_geometry(N):
     """Which K1 variant the fused CG runs (mirrors launch_k1 in cg.cu): box
-    contexts with an even node count 8 <= n = N+1 <= 16 and h2 = 0 form the metric
+    contexts with an even node count 8 <= n = N+1 <= 16 form the metric
     on the fly from the trilinear map (56 B/node + 192 B/element streamed);
     otherwise the 6 stored factors are streamed (104 B/node)."""
     n = N + 1
