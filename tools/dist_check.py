@@ -37,10 +37,14 @@ def main():
     from paper_2109_03592_b200.dist import DistContext
 
     failures = []
-    for (ex, ey, ez, N, deform, tol) in [(8, 8, 8, 7, 0.05, 1e-8), (6, 5, 4, 5, 0.03, 1e-10)]:
-        ctx = DistContext.box(ex, ey, ez, N, deform=deform, device=local)
-        mesh = sb.build_box_mesh(ex, ey, ez, deform=deform)
-        G = O.Problem(ex, ey, ez, N, corners=mesh.corners)
+    F = (False, False, False)
+    cases = [(8, 8, 8, 7, 0.05, 1e-8, F, 0.0), (6, 5, 4, 5, 0.03, 1e-10, F, 0.0),
+             # periodic in x and z (Dirichlet only on the y faces), Helmholtz
+             (6, 4, 4, 7, 0.0, 1e-10, (True, False, True), 1.0)]
+    for (ex, ey, ez, N, deform, tol, per, h2) in cases:
+        ctx = DistContext.box(ex, ey, ez, N, deform=deform, periodic=per, device=local)
+        mesh = sb.build_box_mesh(ex, ey, ez, periodic=per, deform=deform)
+        G = O.Problem(ex, ey, ez, N, periodic=per, corners=mesh.corners)
         n3 = (N + 1) ** 3
         ln = (ctx.local_elements[:, None] * n3 + np.arange(n3)[None, :]).ravel()
         f = O.fill_uniform(99, G.nodes_count)
@@ -50,24 +54,25 @@ def main():
         if not np.array_equal(got.cpu().numpy(), ref[ln]):
             failures.append(f"gs {ex}x{ey}x{ez} N={N}")
         # assembled operator (fast kernels: tolerance), masked
-        op = sb.HelmholtzOperator(ctx, sb.HelmholtzCoeffs(1.0, 0.0))
+        op = sb.HelmholtzOperator(ctx, sb.HelmholtzCoeffs(1.0, h2))
         u = G.rhs_random_continuous(5)
         q = torch.empty(ln.size, dtype=torch.float64, device="cuda")
         op.apply(torch.from_numpy(u[ln]).cuda(), q)
-        qa = G.apply(u, 1.0, 0.0)[ln]
+        qa = G.apply(u, 1.0, h2)[ln]
         err = np.linalg.norm(q.cpu().numpy() - qa) / np.linalg.norm(qa)
         if not err <= 1e-12:
             failures.append(f"apply rel err {err:.2e}")
         # PCG
         b = G.rhs_random_continuous(77)
-        refp = G.pcg(b, 1.0, 0.0, "jacobi", tol, 5000)
+        refp = G.pcg(b, 1.0, h2, "jacobi", tol, 5000)
         x = torch.zeros(ln.size, dtype=torch.float64, device="cuda")
         r = sb.pcg(op, torch.from_numpy(b[ln]).cuda(), x, sb.KrylovConfig(tol, 5000))
         xe = np.linalg.norm(x.cpu().numpy() - refp.x[ln]) / max(np.linalg.norm(refp.x[ln]), 1e-300)
         ok = r.iterations == refp.iterations and xe <= 1e-10 and r.converged
         if not ok:
             failures.append(f"pcg its {r.iterations} vs {refp.iterations}, x err {xe:.2e}")
-        print(f"rank {rank}/{world} box {ex}x{ey}x{ez} N={N}: {ctx.elem_count} elements, "
+        print(f"rank {rank}/{world} box {ex}x{ey}x{ez} N={N} per={per} h2={h2}: "
+              f"{ctx.elem_count} elements, "
               f"pcg {r.iterations} its (ref {refp.iterations}), x err {xe:.2e}, apply err "
               f"{err:.2e}", flush=True)
         ctx.close()
