@@ -471,7 +471,7 @@ def run_ours_dist(args):
                 "e2e": {"value": nodes_global * iters / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,
                         "ms_per_step": e2e_ms, "h2d_bytes_per_step": 2 * 8 * nodes_global,
                         "d2h_bytes_per_step": 8 * nodes_global},
-                "gpu_launches": args.steps * (3 * iters + 7) * world,
+                "gpu_launches": args.steps * (3 * iters + 6) * world,
                 "roofline": roofline_block(N, ctx.elem_count, ctx.nodes,
                                            ax_ms / max(ax_n, 1), up_ms / max(up_n, 1),
                                            ms / iters, peak, peak_kind, None,
