@@ -115,8 +115,8 @@ struct CgK1Pol {
   // esend_off[e0], esend_off[e0 + cnt] a few steps ahead and hands the step's
   // send count to the consumers through the slot metadata
   __device__ static const int32_t* send_index(const Args& a) { return a.esend_off; }
-  // after the element(s) of a step are written: put their interface values in
-  // the send buffer (group-uniform; no-op on a single GPU)
+  // after the element(s) of a step are written: push their interface values
+  // into the neighbours' receive buffers (group-uniform; no-op on one GPU)
   __device__ static void element_done(Args& a, int nsend, int64_t e0, int cnt, int n3, int lt,
                                       int tg, int bar) {
     if (nsend == 0) return;

@@ -148,7 +148,6 @@ __global__ void dist_iface_kernel(DistDev D, int phase, int slot, double* __rest
     }
   }
   const int64_t par = (int64_t)(ld_volatile_u64(D.seq + phase) & 1);
-  // remote copies are pulled from the owners' send buffers over NVLink
   // remote copies were pushed into this rank's receive buffer
   const double* rb = D.recvb + (int64_t)(slot * 2 + par) * D.recv_total;
   const int64_t NL = D.nodes_local;
