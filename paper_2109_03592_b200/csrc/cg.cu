@@ -494,12 +494,15 @@ __global__ void __launch_bounds__(AxCfg<n>::threads)
 // step.  The group width is the smallest multiple of 32 (<= 192) that leaves at
 // most 1/8 of the lanes idle, else the plain round-up (n = 6: 160 threads for
 // 4 elements instead of 64 threads with 28 idle).
+#ifndef SBX_K2_MAXTG
+#define SBX_K2_MAXTG 192  // widest K2 group considered (A/B knob)
+#endif
 template <int n>
 struct K2Geom {
   static constexpr int nn = n * n;
   static constexpr int n3 = n * n * n;
   static constexpr int pick_tg() {
-    for (int tg = ((nn + 31) / 32) * 32; tg <= 192; tg += 32)
+    for (int tg = ((nn + 31) / 32) * 32; tg <= SBX_K2_MAXTG; tg += 32)
       if (8 * (tg - (tg / nn) * nn) <= tg) return tg;
     return ((nn + 31) / 32) * 32;
   }
