@@ -992,6 +992,9 @@ int num_sms(int dev) {
 #ifndef SBX_TRI_G8
 #define SBX_TRI_G8 4
 #endif
+#ifndef SBX_TRI_MINN
+#define SBX_TRI_MINN 8  // smallest n with the trilinear-metric K1 (A/B knob)
+#endif
 #ifndef SBX_TRI_G12
 #define SBX_TRI_G12 2
 #endif
@@ -1051,7 +1054,7 @@ cudaError_t launch_k1(const OpDev& op, const double* r, const double* dinv, doub
     // (measured: pays from n = 8, where the streamed factors dominate the
     // bytes; at n = 6 the kernel turns FP64-latency bound first)
     // (Helmholtz, h2 != 0: the mass term h2*bm*p still streams bm, 8 B/node)
-    const bool tri = n >= 8 && op.tl && !stored && aligned16(op.tl);
+    const bool tri = n >= SBX_TRI_MINN && op.tl && !stored && aligned16(op.tl);
     if (dinv && h2 != 0.0)
       return tri ? launch_k1_tma<n, true, true, true>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev)
                  : launch_k1_tma<n, true, true, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
