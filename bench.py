@@ -62,7 +62,9 @@ def roofline_block(N, E, nodes, k1_ms, k2_ms, it_ms, peak, peak_kind, traffic, k
     stored_cap = peak * 1e9 / 136 / 1e9  # GDOF/s at the stored-geometry HBM bound
     return {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak,
             "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": traffic, "geometry": geo,
+            "traffic": traffic,
+            "traffic_ncu": "profiles/k1_traffic.json (ncu --set full dram bytes per K1 launch)",
+            "geometry": geo,
             "algorithmic_bytes_per_node": k1_bytes / nodes, "k1_ms": k1_ms, "k2_ms": k2_ms,
             "k1_share": k1_ms / max(k1_ms + k2_ms, 1e-12),
             "iteration": {"bytes_per_node": it_bytes / nodes, "achieved_gbs": it_gbs,
@@ -178,9 +180,10 @@ def parse():
     ap.add_argument("--degree", type=int, default=7)
     ap.add_argument("--iters", type=int, default=100, help="CG iterations per step")
     ap.add_argument("--deform", type=float, default=0.05)
-    ap.add_argument("--cpu-sample", type=int, nargs=3, default=[32, 32, 32],
-                    help="mesh of the bounded CPU-baseline sample")
-    ap.add_argument("--cpu-iters", type=int, default=30)
+    ap.add_argument("--ref-iters", type=int, default=6,
+                    help="reference pcg iterations per timed CPU step (bounded sample)")
+    ap.add_argument("--no-one-worker", action="store_true",
+                    help="skip the 1-thread reference figure")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ax-microbench", action="store_true")
     return ap.parse_args()
@@ -194,58 +197,141 @@ def dist_env():
 
 
 # --------------------------------------------------------------- CPU arm --
-def cpu_reference_run(ex, ey, ez, N, deform, iters, steps, warmup):
-    """The reference's pcg (oracle/_ref: sembox compiled unmodified) on all host
-    threads.  Returns per-step seconds and metadata."""
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+_REF_PROBLEM = {}
+
+
+def ref_problem(ex, ey, ez, N, deform):
+    """The reference's own problem (oracle/_ref: sembox compiled unmodified;
+    the C port if the build is absent), with the benchmark right-hand side
+    prepared inside it.  Built once per process (untimed setup)."""
     from oracle import oracle as O
 
-    O.build(ref=True) if not O.ref_available() and os.path.isdir("/root/reference") else None
-    backend = "ref" if O.ref_available() else "port"
+    key = (ex, ey, ez, N, deform)
+    if key not in _REF_PROBLEM:
+        if not O.ref_available() and os.path.isdir("/root/reference"):
+            O.build(ref=True)
+        backend = "ref" if O.ref_available() else "port"
+        cr = O.box_corners(ex, ey, ez, deform=deform)
+        if backend == "ref":
+            O._ref().ref_set_workers(os.cpu_count() or 1)
+        P = O.Problem(ex, ey, ez, N, corners=cr, backend=backend)
+        b = P.rhs_random_continuous(77)
+        if backend == "ref":
+            P.bench_prepare(b)
+            P.drop("inv_mult", "mask")
+        _REF_PROBLEM[key] = (P, b, backend)
+    return _REF_PROBLEM[key]
+
+
+def cpu_reference_run(ex, ey, ez, N, deform, iters, steps, warmup, workers=None):
+    """Times the reference's pcg (krylov.cpp:7-91 with HelmholtzOperator, the
+    parallel Jacobi lambda and the weighted dot) on the SAME mesh as the GPU
+    arm, `iters` iterations per step (tolerance 0), with `workers` host
+    threads (default: all).  Also times the solve's fixed start-up (a
+    0-iteration pcg: b'b, the zero-guess scan, the first preconditioner
+    application and dots) so the per-iteration cost can be separated from it.
+    Returns (step seconds list, startup seconds, backend, threads, nodes)."""
+    from oracle import oracle as O
+
+    P, b, backend = ref_problem(ex, ey, ez, N, deform)
     cores = os.cpu_count() or 1
+    threads = workers or cores
+    if backend == "ref":
+        O._ref().ref_set_workers(threads)
+
+        def solve(k):
+            got = P.bench_solve(k)
+            assert got == k, (got, k)
+    else:
+        threads = 1
+
+        def solve(k):
+            r = P.pcg(b, 1.0, 0.0, "jacobi", 0.0, k)
+            assert r.iterations == k, (r.iterations, k)
+
+    for _ in range(warmup):
+        solve(iters)
+    t0 = time.perf_counter()
+    solve(0)
+    startup = time.perf_counter() - t0
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        solve(iters)
+        times.append(time.perf_counter() - t0)
     if backend == "ref":
         O._ref().ref_set_workers(cores)
-    cr = O.box_corners(ex, ey, ez, deform=deform)
-    P = O.Problem(ex, ey, ez, N, corners=cr, backend=backend)
-    b = P.rhs_random_continuous(77)
-    times = []
-    for s in range(warmup + steps):
-        t0 = time.perf_counter()
-        r = P.pcg(b, 1.0, 0.0, "jacobi", 0.0, iters)
-        dt = time.perf_counter() - t0
-        if s >= warmup:
-            times.append(dt)
-        assert r.iterations == iters, (r.iterations, iters)
-    return times, backend, (cores if backend == "ref" else 1), P.nodes_count
+    return times, startup, backend, threads, P.nodes_count
+
+
+def cpu_summary(times, startup, nodes, iters, full_iters):
+    """Per-iteration cost from the timed steps (step - start-up) / iterations,
+    and the metric for the benchmark's own step (start-up + full_iters
+    iterations), in GDOF/s of local nodes."""
+    t = statistics.median(times)
+    t_it = max(t - startup, 1e-9) / max(iters, 1)
+    full = startup + full_iters * t_it
+    return {"value": nodes * full_iters / full / 1e9,
+            "sample_value": nodes * iters / t / 1e9,
+            "ms_per_iteration": t_it * 1e3, "startup_ms": startup * 1e3,
+            "ms_per_sample_step": t * 1e3}
 
 
 def run_reference_arm(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    ex, ey, ez = args.cpu_sample
+    ex, ey, ez = args.elements
     N = args.degree
-    iters = args.cpu_iters
-    times, backend, cores, nodes = cpu_reference_run(ex, ey, ez, N, args.deform, iters,
-                                                     max(args.steps, 1), 1)
-    t = statistics.median(times)
-    val = nodes * iters / t / 1e9
-    sample = (f"{ex}x{ey}x{ez} deformed box N={N}, {iters} PCG iterations per step "
-              f"(bounded sample of the {args.elements[0]}x{args.elements[1]}x{args.elements[2]} "
-              f"workload; GDOF/s is per local node and iteration)")
+    iters = args.ref_iters
+    t_setup = time.perf_counter()
+    ref_problem(ex, ey, ez, N, args.deform)
+    t_setup = time.perf_counter() - t_setup
+    times, startup, backend, cores, nodes = cpu_reference_run(
+        ex, ey, ez, N, args.deform, iters, max(args.steps, 1), args.warmup)
+    s = cpu_summary(times, startup, nodes, iters, args.iters)
+    # one host thread (BASELINE.md section 3): a bounded 1-iteration sample
+    one = None
+    if backend == "ref" and not args.no_one_worker:
+        t1, st1, _, _, _ = cpu_reference_run(ex, ey, ez, N, args.deform, 1, 1, 0, workers=1)
+        one = cpu_summary(t1, st1, nodes, 1, args.iters)
+        one["cores"] = 1
+    val = s["value"]
+    sample = (f"the {ex}x{ey}x{ez} N={N} bench mesh itself (same config as the GPU arm); each "
+              f"timed step is a {iters}-iteration reference pcg from x=0 (tol 0); value = "
+              f"local nodes x {args.iters} / (start-up + {args.iters} x per-iteration time), "
+              f"i.e. the bench's {args.iters}-iteration step, from the measured start-up "
+              f"({s['startup_ms']:.0f} ms, a 0-iteration pcg) and the measured per-iteration "
+              f"cost ((step - start-up) / {iters})")
     line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": len(times), "warmup": 1, "ms_per_step": t * 1e3,
-            "ms_per_iteration": t * 1e3 / iters, "higher_is_better": True,
+            "steps": len(times), "warmup": args.warmup,
+            "ms_per_step": s["startup_ms"] + args.iters * s["ms_per_iteration"],
+            "ms_per_iteration": s["ms_per_iteration"], "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": "Poisson PCG, Jacobi, deformed box (a=0.05), zero guess",
-                       "elements": list(args.elements), "degree": N,
+                       "elements": [ex, ey, ez], "degree": N,
                        "iterations_per_step": args.iters,
                        "parallelism": f"reference CPU pcg, {cores} host threads",
                        "timed_sample": {"elements": [ex, ey, ez],
-                                        "iterations_per_step": iters}},
+                                        "iterations_per_timed_step": iters},
+                       "setup_s": round(t_setup, 2)},
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores,
                              "kind": "reference" if backend == "ref" else "port",
-                             "sample": sample},
+                             "cpu_model": cpu_model(), "sample": sample,
+                             "sample_value": s["sample_value"],
+                             "ms_per_iteration": s["ms_per_iteration"],
+                             "startup_ms": s["startup_ms"], "one_worker": one},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -330,13 +416,9 @@ def run_ours(args):
     peak, peak_kind = load_peaks()
     k1_ms = ax_ms / max(ax_n, 1)
     k2_ms = up_ms / max(up_n, 1)
+    # DRAM bytes are not measurable in-run without a profiler: traffic stays
+    # null here; the ncu capture of the same kernels is under profiles/
     traffic = None
-    tfile = os.path.join(ROOT, "profiles", "k1_traffic.json")
-    if os.path.exists(tfile):
-        try:
-            traffic = json.load(open(tfile)).get("bytes_per_launch")
-        except Exception:
-            traffic = None
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "ms_per_iteration": ms / iters,
@@ -359,16 +441,18 @@ def run_ours(args):
     if not args.no_ax_microbench:
         line["ax_microbench"] = ax_microbench(peak)
     if not args.no_cpu_baseline:
-        cex, cey, cez = args.cpu_sample
-        times, backend, cores, cnodes = cpu_reference_run(cex, cey, cez, N, args.deform,
-                                                          args.cpu_iters, 1, 0)
-        t = statistics.median(times)
+        # the reference pcg on this box's host cores, same mesh, bounded sample
+        times, startup, backend, cores, cnodes = cpu_reference_run(
+            ex, ey, ez, N, args.deform, args.ref_iters, 1, 0)
+        cs = cpu_summary(times, startup, cnodes, args.ref_iters, iters)
         line["cpu_baseline"] = {
-            "value": cnodes * args.cpu_iters / t / 1e9, "unit": UNIT, "cores": cores,
-            "kind": "reference" if backend == "ref" else "port",
-            "sample": f"{cex}x{cey}x{cez} deformed box N={N}, {args.cpu_iters} PCG iterations "
-                      f"(reference sembox pcg, {cores} threads)",
-            "ms_per_iteration": t * 1e3 / args.cpu_iters}
+            "value": cs["value"], "unit": UNIT, "cores": cores,
+            "kind": "reference" if backend == "ref" else "port", "cpu_model": cpu_model(),
+            "sample": f"{ex}x{ey}x{ez} N={N} (the bench mesh), one {args.ref_iters}-iteration "
+                      f"reference pcg after a 0-iteration start-up probe; value projected to "
+                      f"the {iters}-iteration step (see --impl reference)",
+            "ms_per_iteration": cs["ms_per_iteration"], "startup_ms": cs["startup_ms"]}
+        _REF_PROBLEM.clear()
     print(json.dumps(line), flush=True)
 
 

@@ -245,6 +245,13 @@ sbx_status sbx_ctx_enable_timing(sbx_ctx* ctx, int enable);
 sbx_status sbx_ctx_kernel_time(const sbx_ctx* ctx, const char* name, double* total_ms,
                                int64_t* launches);
 
+/* Test hook (no reference counterpart): one launch of the fused solver's
+ * element kernel K1 in its first-iteration form (p = u, no preconditioner),
+ * so w = D^T G D u h1 + h2 bm u comes out of exactly the kernel -- and the
+ * metric variant (on-the-fly trilinear on box contexts) -- that sbx_pcg
+ * runs.  Single-process contexts only. */
+sbx_status sbx_debug_cg_k1(sbx_ctx* ctx, const double* u, double* w, double h1, double h2);
+
 #ifdef __cplusplus
 }
 #endif

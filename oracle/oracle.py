@@ -144,6 +144,8 @@ def _ref():
         L.ref_pcg.argtypes = [_P, C.c_double, C.c_double, C.c_int, _dp, _dp, C.c_double,
                               C.c_int, _i64p, _dp, _dp, C.c_int64, _i64p]
         L.ref_partition_rcb.argtypes = [_P, C.c_int, _i32p]
+        L.ref_bench_prepare.argtypes = [_P, C.c_double, C.c_double, _dp]
+        L.ref_bench_solve.argtypes = [_P, C.c_int, _i64p, _dp]
         L.ref_dense_helmholtz_element.argtypes = [_P, C.c_int, C.c_double, C.c_double, _dp]
         L.ref_trilinear_point.argtypes = [_P, C.c_int, C.c_double, C.c_double, C.c_double, _dp]
         L.ref_fill_uniform.argtypes = [C.c_uint64, C.c_int64, C.c_double, C.c_double, _dp]
@@ -235,27 +237,44 @@ class Problem:
         self._h = h
         sizes = np.empty(4, np.int64)
         L.ref_problem_sizes(h, sizes)
-        n, N, G = self.n, int(sizes[2]), int(sizes[3])
-        self.global_count = G
+        self.global_count = int(sizes[3])
+        # the reference's arrays are copied out on first use (__getattr__):
+        # at the benchmark size (64^3, N=7) each one is a 1 GB host array
 
-        def dbl(which, count):
+    # reference-owned arrays fetched lazily: name -> (kind, which, count)
+    _REF_ARRAYS = {"nodes": ("d", 0, "n"), "weights": ("d", 1, "n"), "deriv": ("d", 2, "nn"),
+                   "g1": ("d", 3, "N"), "g2": ("d", 4, "N"), "g3": ("d", 5, "N"),
+                   "g4": ("d", 6, "N"), "g5": ("d", 7, "N"), "g6": ("d", 8, "N"),
+                   "bm": ("d", 9, "N"), "jac": ("d", 10, "N"), "mask": ("d", 11, "N"),
+                   "inv_mult": ("d", 12, "N"), "gid": ("i", 0, "N"),
+                   "group_offsets": ("i", 1, "G1"), "group_nodes": ("i", 2, "N"),
+                   "mult": ("m", 0, "N")}
+
+    def __getattr__(self, name):
+        spec = Problem._REF_ARRAYS.get(name)
+        d = self.__dict__
+        if spec is None or d.get("backend") != "ref" or d.get("_h") is None:
+            raise AttributeError(name)
+        kind, which, cnt = spec
+        count = {"n": d["n"], "nn": d["n"] ** 2, "N": d["nodes_count"],
+                 "G1": d["global_count"] + 1}[cnt]
+        L = _ref()
+        if kind == "d":
             a = np.empty(count)
-            L.ref_copy_double(h, which, a)
-            return a
+            L.ref_copy_double(d["_h"], which, a)
+        elif kind == "i":
+            a = np.empty(count, np.int64)
+            L.ref_copy_int64(d["_h"], which, a)
+        else:
+            a = np.empty(count, np.int32)
+            L.ref_copy_mult(d["_h"], a)
+        setattr(self, name, a)
+        return a
 
-        self.nodes, self.weights, self.deriv = dbl(0, n), dbl(1, n), dbl(2, n * n)
-        (self.g1, self.g2, self.g3, self.g4, self.g5, self.g6, self.bm, self.jac) = [
-            dbl(w, N) for w in range(3, 11)]
-        self.mask = dbl(11, N)
-        self.inv_mult = dbl(12, N)
-        self.gid = np.empty(N, np.int64)
-        L.ref_copy_int64(h, 0, self.gid)
-        self.group_offsets = np.empty(G + 1, np.int64)
-        L.ref_copy_int64(h, 1, self.group_offsets)
-        self.group_nodes = np.empty(N, np.int64)
-        L.ref_copy_int64(h, 2, self.group_nodes)
-        self.mult = np.empty(N, np.int32)
-        L.ref_copy_mult(h, self.mult)
+    def drop(self, *names):
+        """Release lazily fetched reference arrays (memory at large sizes)."""
+        for nm in names:
+            self.__dict__.pop(nm, None)
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -337,6 +356,24 @@ class Problem:
                                 h2, pc, b, x, tol, max_iterations, info, res, hist, cap, hlen)
         return PcgOut(int(info[0]), bool(info[1]), float(res[0]), float(res[1]),
                       hist[: min(int(hlen[0]), cap)].copy(), x, int(rc), int(info[2]))
+
+    # -- benchmark session (reference backend only) ------------------------
+    def bench_prepare(self, b, h1=1.0, h2=0.0):
+        """Untimed setup of a timed reference solve: the assembled Jacobi
+        diagonal and the right-hand side stay inside the reference problem."""
+        assert self.backend == "ref"
+        rc = _ref().ref_bench_prepare(self._h, h1, h2, np.ascontiguousarray(b, np.float64))
+        if rc:
+            raise OracleError(rc, _ref().ref_last_error().decode())
+
+    def bench_solve(self, iters):
+        """x = 0, then the reference pcg for exactly `iters` iterations."""
+        info = np.zeros(3, np.int64)
+        res = np.zeros(2)
+        rc = _ref().ref_bench_solve(self._h, iters, info, res)
+        if rc:
+            raise OracleError(rc, _ref().ref_last_error().decode())
+        return int(info[0])
 
     def partition_rcb(self, ranks):
         out = np.empty(self.E, np.int32)

@@ -58,6 +58,10 @@ struct Problem {
   GeometricFactors gf;
   GatherScatterMap map;
   Field mask;
+  // benchmark session (ref_bench_prepare / ref_bench_solve): rhs, solution
+  // and Jacobi diagonal kept here so a timed step is the pcg call itself
+  Field bench_b, bench_x, bench_diag;
+  double bench_h1 = 0.0, bench_h2 = 0.0;
 };
 
 template <typename F>
@@ -284,6 +288,56 @@ int ref_pcg(void* h, double h1, double h2, int precond, const double* b, double*
       throw;
     }
     unwrap(xf, x);
+  });
+}
+
+// Benchmark session, setup part (untimed): the operator's assembled
+// diagonal (HelmholtzOperator::assembled_diagonal, operators.cpp:536-540) and
+// the right-hand side.
+int ref_bench_prepare(void* h, double h1, double h2, const double* b) {
+  auto* p = static_cast<Problem*>(h);
+  return guarded([&] {
+    HelmholtzOperator op{&p->gf, &p->basis, &p->map, &p->mask, {h1, h2, nullptr, nullptr}};
+    p->bench_diag = op.assembled_diagonal();
+    p->bench_b = wrap(*p, b);
+    p->bench_x = Field(GridTag::velocity, p->mesh.elem_count, p->basis.n());
+    p->bench_h1 = h1;
+    p->bench_h2 = h2;
+  });
+}
+
+// Benchmark session, timed part: x = 0 (parallel fill, as the GPU arm zeroes
+// its x on the device), then the reference's own pcg (krylov.cpp:7-91) with
+// HelmholtzOperator::apply, the parallel Jacobi lambda of stepper.cpp:180-185
+// and field_dot_weighted, for exactly `iters` iterations (tolerance 0).
+int ref_bench_solve(void* h, int iters, std::int64_t* info, double* res) {
+  auto* p = static_cast<Problem*>(h);
+  return guarded([&] {
+    HelmholtzOperator op{&p->gf, &p->basis, &p->map, &p->mask,
+                         {p->bench_h1, p->bench_h2, nullptr, nullptr}};
+    const Field& diag = p->bench_diag;
+    const DotFn dot = [&](const Field& a, const Field& bb) {
+      return field_dot_weighted(a, bb, p->map.inv_mult);
+    };
+    const PrecondFn pre = [&](const Field& r, Field& z) {
+      if (!z.same_shape(r)) z = Field(r.tag, r.elem_count, r.n1d);
+      parallel_for_ranges(r.size(), [&](std::int64_t lo, std::int64_t hi) {
+        for (std::int64_t a = lo; a < hi; ++a) z.v[a] = r.v[a] / diag.v[a];
+      });
+    };
+    Field& x = p->bench_x;
+    parallel_for_ranges(x.size(), [&](std::int64_t lo, std::int64_t hi) {
+      for (std::int64_t a = lo; a < hi; ++a) x.v[a] = 0.0;
+    });
+    KrylovConfig cfg;
+    cfg.tolerance = 0.0;
+    cfg.max_iterations = iters;
+    const PcgResult r =
+        pcg([&](const Field& in, Field& o) { op.apply(in, o); }, p->bench_b, pre, dot, cfg, x);
+    info[0] = r.iterations;
+    info[1] = r.converged ? 1 : 0;
+    res[0] = r.rel_residual;
+    res[1] = r.rel_residual_precond;
   });
 }
 

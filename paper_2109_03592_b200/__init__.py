@@ -22,6 +22,7 @@ from .api import (  # noqa: F401
     SpectralBasis,
     axhelm,
     axhelm_diagonal,
+    debug_cg_k1,
     build_box_mesh,
     build_dirichlet_mask,
     build_gather_scatter,

@@ -91,6 +91,7 @@ _sig("sbx_ctx_dist_connect", _i, _vp, _vp)
 _sig("sbx_ctx_local_elements", _i, _vp, _vp)
 _sig("sbx_ctx_enable_timing", _i, _vp, _i)
 _sig("sbx_ctx_kernel_time", _i, _vp, C.c_char_p, C.POINTER(_d), C.POINTER(_i64))
+_sig("sbx_debug_cg_k1", _i, _vp, _vp, _vp, _d, _d)
 
 FLAG_EXACT = 0x1
 FLAG_FLIP_T = 0x2

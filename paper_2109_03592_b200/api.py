@@ -395,6 +395,18 @@ def axhelm(u, coeffs: HelmholtzCoeffs, ctx: Context, out=None, exact=False, flip
     return out
 
 
+def debug_cg_k1(u, coeffs: HelmholtzCoeffs, ctx: Context, out=None):
+    """Test hook: w = A_local u from the fused solver's own element kernel
+    (K1, first-iteration form; the on-the-fly trilinear metric on box
+    contexts).  Same result contract as axhelm (operators.cpp:215-263)."""
+    u = _f64(u)
+    ctx._shape_check(u)
+    if out is None:
+        out = np.empty(ctx.nodes) if isinstance(u, np.ndarray) else u.new_empty(ctx.nodes)
+    _check(lib.sbx_debug_cg_k1(ctx.handle, _ptr(u), _ptr(out), coeffs.h1, coeffs.h2))
+    return out
+
+
 def axhelm_diagonal(coeffs: HelmholtzCoeffs, ctx: Context, assembled=False, device=False):
     """operators.hpp:64-66 / operators.cpp:272-298 (+ gs_sum when assembled)."""
     out = ctx.new_field(device)
@@ -465,6 +477,10 @@ def pcg(op: HelmholtzOperator, b, x, cfg: KrylovConfig = KrylovConfig(),
     raise SolverError(iteration); max_iterations is reported, not raised.
     mode "exact" reproduces the reference bit for bit; "fast" is the fused
     device-resident solver."""
+    if not op.use_mask:
+        # the fused and the reference-order solvers both solve the masked
+        # (Dirichlet) system; the unmasked operator is singular for Poisson
+        raise ContractViolation("pcg: HelmholtzOperator(use_mask=False) is not supported")
     b = _f64(b)
     op.ctx._shape_check(b, x)
     c = L.PcgConfig()

@@ -80,6 +80,10 @@ struct sbx_ctx {
   std::vector<void*> peer_windows;
   // timing
   bool timing = false;
+  // a multi-GPU exchange timed out: the per-phase sequence counters of the
+  // ranks are out of step, so every later call is refused (recreate the
+  // context on every rank)
+  bool poisoned = false;
 };
 
 namespace {
@@ -149,6 +153,10 @@ sbx_status stage_in(sbx_ctx* c, const double* p, int slot, const double** out) {
 // stream, ordered after all work already queued on the caller's stream
 // (default: the legacy default stream, i.e. torch's default stream).
 sbx_status enter(sbx_ctx* c) {
+  if (c->poisoned) {
+    set_error("context unusable after a multi-GPU exchange timeout; recreate it on every rank");
+    return SBX_E_COMM;
+  }
   SBX_CUDA(cudaSetDevice(c->device));
   SBX_CUDA(cudaEventRecord(c->order_ev, c->caller));
   SBX_CUDA(cudaStreamWaitEvent(c->stream, c->order_ev, 0));
@@ -160,6 +168,17 @@ sbx_status finish(sbx_ctx* c) {
   if (e != cudaSuccess) {
     set_error(std::string("kernel execution: ") + cudaGetErrorString(e));
     return SBX_E_CUDA;
+  }
+  if (c->dist && c->dd.status) {
+    // an exchange kernel (halo or scalar all-reduce) timed out on this rank
+    int st = 0;
+    SBX_CUDA(cudaMemcpy(&st, c->dd.status, sizeof(int), cudaMemcpyDeviceToHost));
+    if (st) {
+      c->poisoned = true;
+      set_error("multi-GPU exchange timed out (a peer rank stopped responding); "
+                "the context is unusable, recreate it on every rank");
+      return SBX_E_COMM;
+    }
   }
   return SBX_OK;
 }
@@ -905,7 +924,9 @@ sbx_status sbx_pcg(sbx_ctx* c, const double* b, double* x, const sbx_pcg_config*
     else if (st == SBX_E_NAN)
       set_error("pcg: residual diverged (NaN/Inf) at iteration " +
                 std::to_string(res->error_iteration));
-    else if (st == SBX_E_SHAPE || st == SBX_E_COMM) set_error(c->cg->error());
+    else if (st == SBX_E_SHAPE || st == SBX_E_COMM || st == SBX_E_CONFIG)
+      set_error(c->cg->error());
+    if (st == SBX_E_COMM) c->poisoned = true;
   } else {
     st = pcg_exact(c, db, dx, cfg, res);
   }
@@ -916,6 +937,37 @@ sbx_status sbx_pcg(sbx_ctx* c, const double* b, double* x, const sbx_pcg_config*
     if (st == SBX_OK) st = f;
   }
   return st;
+}
+
+sbx_status sbx_debug_cg_k1(sbx_ctx* c, const double* u, double* w, double h1, double h2) {
+  SBX_TRY(check_ctx(c));
+  if (!u || !w) {
+    set_error("sbx_debug_cg_k1: null field");
+    return SBX_E_INVALID;
+  }
+  if (c->dist) {
+    set_error("sbx_debug_cg_k1: single-process contexts only (K1 pushes the halo)");
+    return SBX_E_CONFIG;
+  }
+  if (h2 != 0.0 && !c->op.bm) {
+    set_error("sbx_debug_cg_k1: h2 != 0 needs the mass factors (bm)");
+    return SBX_E_SHAPE;
+  }
+  SBX_TRY(enter(c));
+  const double* du = nullptr;
+  SBX_TRY(stage_in(c, u, 0, &du));
+  const bool wdev = is_device_ptr(w);
+  double* dw = w;
+  if (!wdev) SBX_TRY(work(c, 1, &dw));
+  const int rc = c->cg->debug_k1(c->op, c->stream, du, dw, h1, h2);
+  if (rc != SBX_OK) {
+    set_error(c->cg->error());
+    return (sbx_status)rc;
+  }
+  if (!wdev)
+    SBX_CUDA(cudaMemcpyAsync(w, dw, sizeof(double) * (size_t)c->op.nodes, cudaMemcpyDeviceToHost,
+                             c->stream));
+  return finish(c);
 }
 
 sbx_status sbx_ctx_enable_timing(sbx_ctx* c, int enable) {
@@ -1112,8 +1164,10 @@ sbx_status sbx_ctx_create_box_dist(const sbx_box_desc* d, const int32_t* rank_of
       set_error("sbx_ctx_create_box_dist: periodic directions need >= 2 elements");
       return SBX_E_CONFIG;
     }
-  if ((d->degree + 1) % 2 != 0 || d->degree > kMaxTemplN) {
-    set_error("sbx_ctx_create_box_dist: the distributed solver needs an odd degree N <= 15");
+  if (d->degree < 1 || d->degree > kMaxTemplN || !dist_k1_supported(d->degree + 1)) {
+    set_error("sbx_ctx_create_box_dist: the distributed solver needs an odd degree N <= 13 "
+              "(its fused K1 pipeline must fit shared memory), got N=" +
+              std::to_string(d->degree));
     return SBX_E_CONFIG;
   }
   auto plan = std::make_unique<DistPlan>();

@@ -18,10 +18,12 @@
 // Reductions are deterministic (fixed block partials, fixed-order final sum).
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <type_traits>
 
 #include "ax_core.cuh"
 #include "ax_tma.cuh"
@@ -976,7 +978,7 @@ bool k1_use_tma(const OpDev& op, const double* r, const double* dinv, const doub
          (h2 == 0.0 || aligned16(op.bm));
 }
 
-int g_num_sms[64] = {};
+std::atomic<int> g_num_sms[64];  // per device; benign idempotent races
 
 int num_sms(int dev) {
   if (!g_num_sms[dev & 63]) {
@@ -1014,7 +1016,7 @@ cudaError_t launch_k1_tma(const OpDev& op, const double* r, const double* dinv, 
   } else {
     using L = TmaLayout<n, Pol::NV, Ch::GROUPS, Ch::S, TRI>;
     auto kern = ax_tma_kernel<n, Pol, Ch::GROUPS, Ch::S, TRI>;
-    static bool attr_set[64] = {};
+    static std::atomic<bool> attr_set[64];  // per device (distinct contexts may race: idempotent)
     if (!attr_set[dev & 63]) {
       cudaError_t err =
           cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::smem);
@@ -1055,19 +1057,25 @@ cudaError_t launch_k1(const OpDev& op, const double* r, const double* dinv, doub
     // bytes; at n = 6 the kernel turns FP64-latency bound first)
     // (Helmholtz, h2 != 0: the mass term h2*bm*p still streams bm, 8 B/node)
     const bool tri = n >= SBX_TRI_MINN && op.tl && !stored && aligned16(op.tl);
-    if (dinv && h2 != 0.0)
-      return tri ? launch_k1_tma<n, true, true, true>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev)
-                 : launch_k1_tma<n, true, true, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
-    if (h2 != 0.0)
-      return tri ? launch_k1_tma<n, false, true, true>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev)
-                 : launch_k1_tma<n, false, true, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
-    if (dinv)
-      return tri ? launch_k1_tma<n, true, false, true>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev)
-                 : launch_k1_tma<n, true, false, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
-    return tri ? launch_k1_tma<n, false, false, true>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev)
-               : launch_k1_tma<n, false, false, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
+    auto go = [&](auto tri_c) {
+      constexpr bool T = decltype(tri_c)::value;
+      if (dinv && h2 != 0.0)
+        return launch_k1_tma<n, true, true, T>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
+      if (h2 != 0.0)
+        return launch_k1_tma<n, false, true, T>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
+      if (dinv)
+        return launch_k1_tma<n, true, false, T>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
+      return launch_k1_tma<n, false, false, T>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
+    };
+    // a pipeline layout that does not fit shared memory (large n with many
+    // staged vectors) reports NotSupported before launching anything: try the
+    // stored-geometry pipeline, then the per-element-block kernel below
+    cudaError_t e = cudaErrorNotSupported;
+    if (tri) e = go(std::true_type{});
+    if (e == cudaErrorNotSupported) e = go(std::false_type{});
+    if (e != cudaErrorNotSupported || op.dd) return e;
   }
-  static bool attr_set[64] = {};
+  static std::atomic<bool> attr_set[64];  // per device (distinct contexts may race: idempotent)
   if (!attr_set[dev & 63]) {
     cudaError_t err = cudaFuncSetAttribute(
         cg_ax_kernel<n>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem);
@@ -1094,7 +1102,7 @@ cudaError_t launch_k2(const OpDev& op, const double* w, double* r, const double*
     using L = K2Layout<n, Ch::GROUPS, Ch::SPG>;
     auto kern = op.table ? cg_update_tma_kernel<n, Ch::GROUPS, Ch::SPG, true>
                          : cg_update_tma_kernel<n, Ch::GROUPS, Ch::SPG, false>;
-    static bool attr_set[2][64] = {};
+    static std::atomic<bool> attr_set[2][64];
     int dev = 0;
     cudaGetDevice(&dev);
     if (!attr_set[op.table][dev & 63]) {
@@ -1111,9 +1119,12 @@ cudaError_t launch_k2(const OpDev& op, const double* w, double* r, const double*
                                                      partials, hist, hist_cap, cond, use_cond);
     return cudaGetLastError();
   }
+  // multi-GPU: only the table-driven TMA kernel knows remote neighbours (-2),
+  // local element renumbering and the cross-rank r'z / r'r exchange
+  if (op.dd) return cudaErrorNotSupported;
   if (op.box) {
     using C = AxCfg<n>;
-    static int per_sm[64] = {};
+    static std::atomic<int> per_sm[64];
     int dev = 0;
     cudaGetDevice(&dev);
     if (!per_sm[dev & 63]) {
@@ -1139,6 +1150,16 @@ cudaError_t launch_k2(const OpDev& op, const double* w, double* r, const double*
       op.b_off, op.b_idx, op.nB, nBblocks, op.E, w, r, dinv, sc, partials, hist, hist_cap, cond,
       use_cond);
   return cudaGetLastError();
+}
+
+template <int n>
+bool dist_k1_ok() {
+  if constexpr (n % 2 != 0) {
+    return false;
+  } else {
+    return (TmaChoice<n, 3, true, tri_max_groups(n)>::ok || TmaChoice<n, 3, false>::ok) &&
+           (TmaChoice<n, 4, true, tri_max_groups(n)>::ok || TmaChoice<n, 4, false>::ok);
+  }
 }
 
 int64_t k1_blocks(const OpDev& op) {
@@ -1192,6 +1213,19 @@ cudaError_t k2(const OpDev& op, const double* w, double* r, const double* dinv, 
 #undef CALL2
   return err;
 }
+
+}  // namespace
+
+bool dist_k1_supported(int n) {
+  bool ok = false;
+  cudaError_t err = cudaSuccess;
+#define CALL3(NN) ok = dist_k1_ok<NN>()
+  SBX_N_SWITCH(n, CALL3)
+#undef CALL3
+  return ok && err == cudaSuccess;
+}
+
+namespace {
 
 unsigned blocks_for(int64_t work, int threads, int64_t cap) {
   int64_t b = (work + threads - 1) / threads;
@@ -1334,6 +1368,14 @@ int CgEngine::build_graph(const CgRun& run) {
   }
   cudaGraph_t captured = nullptr;
   cudaError_t e3 = cudaStreamEndCapture(run.stream, &captured);
+  if (e1 == cudaErrorNotSupported || e2 == cudaErrorNotSupported) {
+    // only reachable on a distributed context: no pipelined K1/K2 layout
+    // fits shared memory for this degree and coefficient set
+    cudaGetLastError();
+    err_ = "pcg: no fused multi-GPU kernel fits this degree / coefficient combination (N=" +
+           std::to_string(op.n - 1) + ", h2 " + (run.h2 != 0.0 ? "!= 0" : "= 0") + ")";
+    return SBX_E_CONFIG;
+  }
   CG_CUDA(e1);
   CG_CUDA(e2);
   CG_CUDA(e3);
@@ -1486,8 +1528,10 @@ int CgEngine::solve(const CgRun& run, sbx_pcg_result* res) {
       if (run_timed_loop(run) != SBX_OK) return SBX_E_CUDA;
     } else {
       const Key k{run.op, run.x, run.dinv, run.h1, run.h2, hist_, run.stream};
-      if (!have_graph_ || !(k == key_))
-        if (build_graph(run) != SBX_OK) return SBX_E_CUDA;
+      if (!have_graph_ || !(k == key_)) {
+        const int rc = build_graph(run);
+        if (rc != SBX_OK) return rc;
+      }
       CG_CUDA(cudaGraphLaunch(exec_, s));
     }
     cg_finish_kernel<<<(unsigned)std::min<int64_t>((N + 255) / 256, 148 * 16), 256, 0, s>>>(
@@ -1515,6 +1559,32 @@ int CgEngine::solve(const CgRun& run, sbx_pcg_result* res) {
     err_ = "multi-GPU exchange timed out (a peer rank stopped responding)";
     return SBX_E_COMM;
   }
+  return SBX_OK;
+}
+
+int CgEngine::debug_k1(const OpDev& op, cudaStream_t s, const double* u, double* w, double h1,
+                       double h2) {
+  CgRun run;
+  run.op = &op;
+  run.stream = s;
+  run.max_it = 1;
+  if (ensure(run) != SBX_OK) return SBX_E_CUDA;
+  CgScalars h{};
+  h.first = 1;
+  h.max_it = 1;
+  h.err_it = -1;
+  h.nranks = 1;
+  *hsc_ = h;
+  CG_CUDA(cudaMemcpyAsync(sc_, hsc_, sizeof(CgScalars), cudaMemcpyHostToDevice, s));
+  // x is staged by the pipelined K1 but not read or written on the first
+  // iteration: point it at the (unused here) residual buffer
+  const cudaError_t e = k1(op, u, nullptr, p_, r_, w, h1, h2, sc_, partials_, s);
+  if (e == cudaErrorNotSupported) {
+    err_ = "debug_k1: no K1 variant for this context";
+    return SBX_E_CONFIG;
+  }
+  CG_CUDA(e);
+  CG_CUDA(cudaStreamSynchronize(s));
   return SBX_OK;
 }
 

@@ -39,6 +39,11 @@ class CgEngine {
   int solve(const CgRun& run, sbx_pcg_result* res);
   const std::string& error() const { return err_; }
   int kernel_time(const char* name, double* total_ms, int64_t* launches) const;
+  // Test hook: one launch of the solver's K1 in its first-iteration form
+  // (p = r, no preconditioner, x untouched) on u, so w = A_local u comes out
+  // of exactly the kernel (and metric variant) the solve runs.
+  int debug_k1(const OpDev& op, cudaStream_t s, const double* u, double* w, double h1,
+               double h2);
 
  private:
   int ensure(const CgRun& run);

@@ -37,12 +37,14 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
-// Publication rule: values are made visible at GPU scope (__threadfence; every
-// peer access to this rank's memory goes through this GPU's L2), then ONE
-// thread releases a flag with st.release.sys, whose cumulativity orders every
-// write it has observed -- including its own stores into peer mailboxes --
-// before the flag.  Readers acquire the flag with ld.acquire.sys.  No
-// system-scope fence (MEMBAR.SYS) is taken on the hot path.
+// Publication rule: local values are made visible at GPU scope (__threadfence;
+// every peer access to this rank's memory goes through this GPU's L2).  A
+// thread that stored into PEER memory (halo values over NVLink) takes one
+// system-scope fence (__threadfence_system) after its last such store, before
+// its CTA's ticket -- once per storing thread per kernel, not per store.  ONE
+// thread then releases a flag with st.release.sys, whose cumulativity orders
+// every write it has observed -- including its own stores into peer mailboxes
+// -- before the flag.  Readers acquire the flag with ld.acquire.sys.
 __device__ __forceinline__ void dist_fence() { __threadfence(); }
 
 __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {

@@ -159,6 +159,10 @@ cudaError_t launch_pack_geometry(const OpDev& op, const double* const* g_soa, do
 cudaError_t launch_recip(int64_t N, const double* d, double* dinv, cudaStream_t s);
 
 // ---- fused FAST CG (cg.cu) -------------------------------------------------
+// Whether the multi-GPU solver has a pipelined K1 (the halo leaves from its
+// epilogue) for n = N+1 points per direction: Poisson with and without
+// Jacobi (the trilinear or the stored-geometry layout must fit shared memory).
+bool dist_k1_supported(int n);
 struct CgVecs {
   double* x;
   double* r;

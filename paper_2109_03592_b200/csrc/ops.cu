@@ -6,6 +6,7 @@
 // so their output is bitwise equal to sembox built for x86-64.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstdlib>
 
@@ -145,7 +146,7 @@ cudaError_t launch_ax_tma(const OpDev& op, const double* u, double* w, double h1
   } else {
     using L = TmaLayout<n, Pol::NV, Ch::GROUPS, Ch::S>;
     auto kern = ax_tma_kernel<n, Pol, Ch::GROUPS, Ch::S>;
-    static bool attr_set[64] = {};
+    static std::atomic<bool> attr_set[64];  // per device (distinct contexts may race: idempotent)
     int dev = 0;
     cudaGetDevice(&dev);
     if (!attr_set[dev & 63]) {
@@ -154,14 +155,19 @@ cudaError_t launch_ax_tma(const OpDev& op, const double* u, double* w, double h1
       if (err != cudaSuccess) return err;
       attr_set[dev & 63] = true;
     }
-    static int sms[64] = {};
-    if (!sms[dev & 63]) cudaDeviceGetAttribute(&sms[dev & 63], cudaDevAttrMultiProcessorCount, dev);
+    static std::atomic<int> sms[64];
+    if (!sms[dev & 63]) {
+      int v = 0;
+      cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+      sms[dev & 63] = v;
+    }
     DParam<n> Dp;
     for (int q = 0; q < n * n; ++q) Dp.d[q] = op.Dh[q];
     QParam<n> Qp{};
     typename Pol::Args a{u, op.bm, w, h2};
     const int64_t NG = (op.E + TmaGeom<n>::EPG - 1) / TmaGeom<n>::EPG;
-    int64_t grid = sms[dev & 63] > 0 ? sms[dev & 63] : 148;
+    const int nsm = sms[dev & 63];
+    int64_t grid = nsm > 0 ? nsm : 148;
     if (grid > NG) grid = NG;
     kern<<<(unsigned)grid, L::threads, L::smem, s>>>(a, op.G, op.E, h1, tsign, Dp, nullptr, Qp);
     return cudaGetLastError();
@@ -181,7 +187,7 @@ cudaError_t launch_ax_t(const OpDev& op, const double* u, double* w, double h1, 
                                     : launch_ax_tma<n, false>(op, u, w, h1, h2, tsign, s);
     if (e != cudaErrorNotSupported) return e;
   }
-  static bool attr_set[64] = {};
+  static std::atomic<bool> attr_set[64];  // per device (distinct contexts may race: idempotent)
   int dev = 0;
   cudaGetDevice(&dev);
   if (!attr_set[dev & 63]) {
