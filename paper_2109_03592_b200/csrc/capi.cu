@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -593,6 +594,84 @@ sbx_status upload_trilinear(sbx_ctx* c, int degree, const double* corners, int64
   return SBX_OK;
 }
 
+// Device-side setup of a structured box: geometry, mask
+// and multiplicities are built by kernels (setup_dev.cu) from the element
+// corners; the gather-scatter runs on the lattice, so no map is built or
+// uploaded.  Bitwise equal to the host builders (tests/test_gpu_setup.py).
+static sbx_status ctx_setup_box_device(sbx_ctx* c, const sbx_box_desc* d, const double* corners) {
+  const int64_t E = (int64_t)d->ex * d->ey * d->ez;
+  const int n = d->degree + 1;
+  const int64_t N = E * n * n * n;
+  if (N >= (int64_t)INT32_MAX) {
+    set_error("sbx_ctx_create_box: more than 2^31-1 local nodes per device");
+    return SBX_E_SHAPE;
+  }
+  OpDev& op = c->op;
+  op.E = E;
+  op.n = n;
+  op.nodes = N;
+  std::vector<double> x(n), w(n), deriv(n * n);
+  SBX_TRY(sbx_gll_basis(d->degree, x.data(), w.data(), deriv.data()));
+  for (int q = 0; q < n * n; ++q) op.Dh[q] = deriv[q];
+  double* dD = nullptr;
+  SBX_TRY(dupload(c, &dD, deriv.data(), (int64_t)n * n));
+  op.Dd = dD;
+  // corners -> packed G and bm (temporary device copy of the corners)
+  double* dcr = nullptr;
+  SBX_CUDA(cudaMalloc(&dcr, sizeof(double) * (size_t)E * 24));
+  SBX_CUDA(cudaMemcpyAsync(dcr, corners, sizeof(double) * (size_t)E * 24,
+                           cudaMemcpyHostToDevice, c->stream));
+  double *G = nullptr, *bm = nullptr;
+  SBX_TRY(dupload<double>(c, &G, nullptr, 6 * N));
+  SBX_TRY(dupload<double>(c, &bm, nullptr, N));
+  unsigned long long* dbad = reinterpret_cast<unsigned long long*>(c->dcount);
+  SBX_CUDA(cudaMemsetAsync(dbad, 0xff, sizeof(unsigned long long), c->stream));
+  SBX_CUDA(launch_geom_box(dcr, E, n, x.data(), w.data(), G, bm, dbad, c->stream));
+  unsigned long long hbad = 0;
+  SBX_CUDA(cudaMemcpyAsync(&hbad, dbad, sizeof(hbad), cudaMemcpyDeviceToHost, c->stream));
+  SBX_CUDA(cudaMemsetAsync(c->dcount, 0, 64 * sizeof(uint32_t), c->stream));
+  SBX_CUDA(cudaStreamSynchronize(c->stream));
+  cudaFree(dcr);
+  if (hbad != ~0ull) {
+    set_error("build_geometric_factors: nonpositive Jacobian in element " +
+              std::to_string(hbad));
+    return SBX_E_MESH;
+  }
+  op.G = G;
+  op.bm = bm;
+  // lattice: box dims, mask, multiplicities
+  op.box = true;
+  op.lat = true;
+  op.ex = d->ex;
+  op.ey = d->ey;
+  op.ez = d->ez;
+  int64_t gcount = 1;
+  for (int q = 0; q < 3; ++q) {
+    op.per[q] = d->periodic[q] ? 1 : 0;
+    const int64_t span = (int64_t)(q == 0 ? d->ex : q == 1 ? d->ey : d->ez) * d->degree;
+    gcount *= op.per[q] ? span : span + 1;
+  }
+  c->global_count = gcount;
+  double *mask = nullptr, *im = nullptr;
+  uint8_t* m8 = nullptr;
+  SBX_TRY(dupload<double>(c, &mask, nullptr, N));
+  SBX_TRY(dupload<double>(c, &im, nullptr, N));
+  SBX_TRY(dupload<uint8_t>(c, &m8, nullptr, N));
+  SBX_CUDA(launch_lattice_fields(op, mask, im, m8, c->stream));
+  op.mask = mask;
+  op.inv_mult = im;
+  op.mult8 = m8;
+  c->has_mask = true;
+  c->interior_clean = true;  // element-interior nodes: unmasked singletons
+  op.nB = 0;
+  op.nBcopies = 0;
+  SBX_TRY(upload_trilinear(c, d->degree, corners, E));
+  SBX_TRY(ensure_partials(c, std::max<int64_t>(E, 4096)));
+  c->cg.reset(new CgEngine());
+  SBX_CUDA(cudaStreamSynchronize(c->stream));
+  return SBX_OK;
+}
+
 sbx_status sbx_ctx_create_box(const sbx_box_desc* d, int device, sbx_ctx** out) {
   if (!d || !out) {
     set_error("sbx_ctx_create_box: null argument");
@@ -608,6 +687,25 @@ sbx_status sbx_ctx_create_box(const sbx_box_desc* d, int device, sbx_ctx** out) 
   std::vector<double> corners(E * 24);
   SBX_TRY(sbx_box_corners(d->ex, d->ey, d->ez, d->origin, d->lengths, corners.data()));
   if (d->deform_amplitude != 0.0) deform_corners(E, d->deform_amplitude, corners.data());
+  // device-side setup unless disabled (SBX_HOST_SETUP) or the lattice
+  // gather-scatter does not apply (a periodic direction with one element)
+  static const bool host_setup = std::getenv("SBX_HOST_SETUP") != nullptr;
+  bool lattice_ok = true;
+  const int counts[3] = {d->ex, d->ey, d->ez};
+  for (int q = 0; q < 3; ++q)
+    if (d->periodic[q] && counts[q] < 2) lattice_ok = false;
+  if (!host_setup && lattice_ok) {
+    *out = nullptr;
+    auto* c = new sbx_ctx();
+    sbx_status st = ctx_init_common(c, device);
+    if (st == SBX_OK) st = ctx_setup_box_device(c, d, corners.data());
+    if (st != SBX_OK) {
+      sbx_ctx_destroy(c);
+      return st;
+    }
+    *out = c;
+    return SBX_OK;
+  }
   std::vector<double> deriv(n * n);
   SBX_TRY(sbx_gll_basis(d->degree, nullptr, nullptr, deriv.data()));
   std::vector<std::vector<double>> g(7, std::vector<double>(N));
@@ -634,11 +732,7 @@ sbx_status sbx_ctx_create_box(const sbx_box_desc* d, int device, sbx_ctx** out) 
   SBX_TRY(sbx_ctx_create(&pd, device, out));
   SBX_TRY(upload_trilinear(*out, d->degree, corners.data(), E));
   // structured element-centric gather-scatter (needs >= 2 cells per periodic axis)
-  const int counts[3] = {d->ex, d->ey, d->ez};
-  bool ok = true;
-  for (int q = 0; q < 3; ++q)
-    if (d->periodic[q] && counts[q] < 2) ok = false;
-  if (ok) {
+  if (lattice_ok) {
     (*out)->op.box = true;
     (*out)->op.ex = d->ex;
     (*out)->op.ey = d->ey;

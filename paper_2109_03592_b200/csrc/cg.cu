@@ -27,6 +27,7 @@
 
 #include "ax_core.cuh"
 #include "ax_tma.cuh"
+#include "ax_dmma.cuh"
 #include "cg.cuh"
 #include "dist_kern.cuh"
 #include "sbx_internal.h"
@@ -139,6 +140,30 @@ struct CgK1Pol {
     }
     a.p[idx] = u;
     hb = HAS_BM ? a.h2 * v[QB] : 0.0;
+  }
+  // two adjacent nodes (idx even: 16-byte aligned stores), for k1_dmma_kernel
+  __device__ static void pro2(const Args& a, const double (&va)[NV], const double (&vb)[NV],
+                              int64_t idx, double& u0, double& u1, double& h0, double& h1) {
+    const double z0 = HAS_DINV ? va[0] * va[QD] : va[0];
+    const double z1 = HAS_DINV ? vb[0] * vb[QD] : vb[0];
+    if (a.first) {
+      u0 = z0;
+      u1 = z1;
+    } else {
+      u0 = fma(a.beta, va[1], z0);
+      u1 = fma(a.beta, vb[1], z1);
+      stg2(a.x + idx, fma(a.ap, va[1], va[2]), fma(a.ap, vb[1], vb[2]));
+    }
+    stg2(a.p + idx, u0, u1);
+    h0 = h1 = 0.0;
+  }
+  __device__ static void epi2(const Args& a, double acc0, double acc1, double u0, double u1,
+                              double hb0, double hb1, int64_t idx, double& red) {
+    const double w0 = HAS_BM ? fma(hb0, u0, acc0) : acc0;
+    const double w1 = HAS_BM ? fma(hb1, u1, acc1) : acc1;
+    stg2(a.w + idx, w0, w1);
+    red = fma(u0, w0, red);
+    red = fma(u1, w1, red);
   }
   __device__ static double hb_of(const Args& a, double bm) { return a.h2 * bm; }
   __device__ static void epi(const Args& a, double acc, double u, double hb, int64_t idx,
@@ -1040,6 +1065,40 @@ cudaError_t launch_k1_tma(const OpDev& op, const double* r, const double* dinv, 
   }
 }
 
+// K1 on the FP64 tensor cores (n = 8, trilinear metric): ax_dmma.cuh
+template <bool HAS_DINV, bool HAS_BM>
+cudaError_t launch_k1_dmma(const OpDev& op, const double* r, const double* dinv, double* p,
+                           double* x, double* w, double h1, double h2, CgScalars* sc,
+                           double* partials, cudaStream_t s, int dev) {
+  using Pol = CgK1Pol<HAS_DINV, HAS_BM>;
+  using Ch = DmmaChoice<Pol::NV>;
+  if constexpr (!Ch::ok) {
+    return cudaErrorNotSupported;
+  } else {
+    using L = DmmaLayout<Pol::NV, Ch::GROUPS, Ch::SPG>;
+    auto kern = k1_dmma_kernel<Pol, Ch::GROUPS, Ch::SPG>;
+    static std::atomic<bool> attr_set[64];
+    if (!attr_set[dev & 63]) {
+      cudaError_t err =
+          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::smem);
+      if (err != cudaSuccess) return err;
+      attr_set[dev & 63] = true;
+    }
+    DParam<8> Dp;
+    for (int q = 0; q < 64; ++q) Dp.d[q] = op.Dh[q];
+    QParam<8> Qp;
+    for (int q = 0; q < 8; ++q) {
+      Qp.x[q] = op.Xh[q];
+      Qp.w[q] = op.Wh[q];
+    }
+    typename Pol::Args a{r, dinv, p, x, w, op.bm, h2, sc, op.dd, 0.0, 0.0, 0, 0, nullptr, 0};
+    int64_t grid = num_sms(dev);
+    if (grid > op.E) grid = op.E;
+    kern<<<(unsigned)grid, L::threads, L::smem, s>>>(a, op.tl, op.E, h1, Dp, partials, Qp);
+    return cudaGetLastError();
+  }
+}
+
 template <int n>
 cudaError_t launch_k1(const OpDev& op, const double* r, const double* dinv, double* p, double* x,
                       double* w, double h1, double h2, CgScalars* sc, double* partials,
@@ -1071,7 +1130,21 @@ cudaError_t launch_k1(const OpDev& op, const double* r, const double* dinv, doub
     // staged vectors) reports NotSupported before launching anything: try the
     // stored-geometry pipeline, then the per-element-block kernel below
     cudaError_t e = cudaErrorNotSupported;
-    if (tri) e = go(std::true_type{});
+    // n = 8 trilinear: the DMMA kernel unless SBX_K1_FMA selects the FMA one
+    static const bool fma_k1 = std::getenv("SBX_K1_FMA") != nullptr;
+    if constexpr (n == 8) {
+      if (tri && !fma_k1) {
+        if (dinv && h2 != 0.0)
+          e = launch_k1_dmma<true, true>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
+        else if (h2 != 0.0)
+          e = launch_k1_dmma<false, true>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
+        else if (dinv)
+          e = launch_k1_dmma<true, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
+        else
+          e = launch_k1_dmma<false, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
+      }
+    }
+    if (tri && e == cudaErrorNotSupported) e = go(std::true_type{});
     if (e == cudaErrorNotSupported) e = go(std::false_type{});
     if (e != cudaErrorNotSupported || op.dd) return e;
   }
@@ -1430,7 +1503,9 @@ int CgEngine::solve(const CgRun& run, sbx_pcg_result* res) {
   // (checked on this rank's shared groups; cross-rank continuity is the
   // caller's contract in the distributed case)
   CG_CUDA(cudaMemsetAsync(flag_, 0, sizeof(int), s));
-  if (op.nB > 0)
+  if (op.lat)
+    CG_CUDA(launch_check_rhs_box(op, run.b, flag_, s));
+  else if (op.nB > 0)
     cg_check_rhs_kernel<<<(unsigned)((op.nB + 255) / 256), 256, 0, s>>>(op.b_off, op.b_idx,
                                                                         op.nB, run.b, flag_);
   // initial residual: r = b - A x0, the apply skipped for a zero guess

@@ -46,6 +46,9 @@ struct OpDev {
   // kernel can form the metric at each node instead of streaming G
   const double* tl = nullptr;
   double Xh[33], Wh[33];
+  // lattice gather-scatter: mask / multiplicities / gs / rhs check derived
+  // from the box lattice on the device (setup_dev.cu); no boundary CSR
+  bool lat = false;
 };
 
 // Device-resident CG scalars for the fused (FAST) solver.
@@ -157,6 +160,17 @@ cudaError_t launch_mul(int64_t N, const double* a, double* b, cudaStream_t s);
 cudaError_t launch_pack_geometry(const OpDev& op, const double* const* g_soa, double* G,
                                  cudaStream_t s);
 cudaError_t launch_recip(int64_t N, const double* d, double* dinv, cudaStream_t s);
+
+// ---- device-side setup of box contexts (setup_dev.cu) ----------------------
+// packed geometry G [E][6][n^3] and bm from the element corners [E][8][3];
+// *bad = smallest element with detJ <= 0 (initialise to ~0ull)
+cudaError_t launch_geom_box(const double* corners, int64_t E, int n, const double* x,
+                            const double* w, double* G, double* bm, unsigned long long* bad,
+                            cudaStream_t s);
+cudaError_t launch_lattice_fields(const OpDev& op, double* mask, double* inv_mult,
+                                  uint8_t* mult8, cudaStream_t s);
+cudaError_t launch_gs_box(const OpDev& op, double* f, bool apply_mask, cudaStream_t s);
+cudaError_t launch_check_rhs_box(const OpDev& op, const double* f, int* flag, cudaStream_t s);
 
 // ---- fused FAST CG (cg.cu) -------------------------------------------------
 // Whether the multi-GPU solver has a pipelined K1 (the halo leaves from its

@@ -8,6 +8,12 @@
 
 #include <cstdint>
 
+#ifdef __CUDACC__
+#define SBX_HD __host__ __device__
+#else
+#define SBX_HD
+#endif
+
 namespace sbx {
 
 struct AxisOpts {
@@ -22,7 +28,7 @@ struct Lattice {
   bool per[3];
   int64_t gdim[3];
 
-  void init(int ex, int ey, int ez, const int* periodic, int degree) {
+  SBX_HD void init(int ex, int ey, int ez, const int* periodic, int degree) {
     counts[0] = ex;
     counts[1] = ey;
     counts[2] = ez;
@@ -34,7 +40,7 @@ struct Lattice {
     }
   }
 
-  AxisOpts opts(int d, int64_t g) const {
+  SBX_HD AxisOpts opts(int d, int64_t g) const {
     AxisOpts o;
     const int64_t span = static_cast<int64_t>(counts[d]) * N;
     if (g % N != 0) {
@@ -64,7 +70,7 @@ struct Lattice {
   }
 
   // lattice coordinate of local index loc in cell c along d
-  int64_t coord(int d, int64_t c, int loc) const {
+  SBX_HD int64_t coord(int d, int64_t c, int loc) const {
     int64_t g = c * N + loc;
     if (per[d]) g %= gdim[d];
     return g;
@@ -73,7 +79,7 @@ struct Lattice {
   // All copies (global element, local node index within the element) of the
   // lattice point (g0, g1, g2), sorted in the reference's canonical order
   // (ascending global local-node index).  Returns the count (<= 8).
-  int copies(int64_t g0, int64_t g1, int64_t g2, int64_t* elem, int* lidx) const {
+  SBX_HD int copies(int64_t g0, int64_t g1, int64_t g2, int64_t* elem, int* lidx) const {
     const int n = N + 1;
     const AxisOpts o0 = opts(0, g0), o1 = opts(1, g1), o2 = opts(2, g2);
     int64_t key[8];

@@ -441,6 +441,7 @@ cudaError_t launch_axhelm_diag(const OpDev& op, double h1, double h2, double* di
 }
 
 cudaError_t launch_gs(const OpDev& op, double* f, bool apply_mask, cudaStream_t s) {
+  if (op.lat) return launch_gs_box(op, f, apply_mask, s);
   if (op.nB == 0) return cudaSuccess;
   gs_kernel<<<(unsigned)((op.nB + 255) / 256), 256, 0, s>>>(op.b_off, op.b_idx, op.nB, f,
                                                             apply_mask ? 1 : 0);

@@ -1,0 +1,211 @@
+// Device-side setup of a structured-box context: the
+// geometric factors, the Dirichlet mask, the multiplicities, and the
+// gather-scatter over the node lattice, built on the GPU instead of on the
+// host and uploaded.
+//
+// * geom_box_kernel: one thread per node, the node metric of the element's
+//   trilinear map (metric.h, shared with the host builder; this file is
+//   compiled with -fmad=false so every operation rounds as in the reference,
+//   operators.cpp:123-178) written straight into the packed [E][6][n^3]
+//   layout the kernels stream, plus bm; the first element with detJ <= 0 is
+//   reported like the host builder's MeshError.
+// * lattice_fields_kernel: mask (operators.cpp:433-455), inv_mult and the
+//   clamped multiplicity per node from the lattice coordinates
+//   (gather.cpp:15-46 read backwards, lattice.h).
+// * gs_box_kernel: gs_sum_inplace (gather.cpp:85-98) without a CSR: the
+//   thread of a group's FIRST copy (ascending local index) sums the copies
+//   from 0.0 in the reference order and writes every copy; bitwise equal to
+//   the CSR gs_kernel.  Masked copies get s*0.0 when the mask is applied.
+// * check_rhs_box_kernel: the fused CG's continuity / mask precondition on
+//   the right-hand side, per node against its partner copies.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.cuh"
+#include "lattice.h"
+#include "metric.h"
+
+namespace sbx {
+
+namespace {
+
+struct GllParam {
+  double x[33];
+  double w[33];
+};
+
+__global__ void geom_box_kernel(const double* __restrict__ corners, int64_t E, int n,
+                                GllParam q, double* __restrict__ G, double* __restrict__ bm,
+                                unsigned long long* __restrict__ bad) {
+  const int n3 = n * n * n;
+  const int64_t nodes = E * n3;
+  for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < nodes;
+       a += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = a / n3;
+    const int l = (int)(a - e * n3);
+    const int i = l % n, j = (l / n) % n, k = l / (n * n);
+    double cr[24];
+#pragma unroll
+    for (int c = 0; c < 24; ++c) cr[c] = __ldg(corners + e * 24 + c);
+    Metric m;
+    const double wq = q.w[i] * q.w[j] * q.w[k];
+    if (!node_metric(cr, q.x[i], q.x[j], q.x[k], wq, m)) {
+      atomicMin(bad, (unsigned long long)e);
+      continue;
+    }
+    double* Ge = G + e * 6 * (int64_t)n3 + l;
+#pragma unroll
+    for (int c = 0; c < 6; ++c) Ge[c * n3] = m.g[c];
+    if (bm) bm[a] = m.wdet;
+  }
+}
+
+struct BoxLat {
+  int ex, ey, ez;
+  int per[3];
+  int N;
+};
+
+__device__ __forceinline__ Lattice make_lattice(const BoxLat& b) {
+  Lattice L;
+  const int p[3] = {b.per[0], b.per[1], b.per[2]};
+  L.init(b.ex, b.ey, b.ez, p, b.N);
+  return L;
+}
+
+// lattice coordinates of local node a
+__device__ __forceinline__ void node_coords(const Lattice& L, const BoxLat& b, int64_t a,
+                                            int64_t g[3], bool& boundary) {
+  const int n = b.N + 1, n3 = n * n * n;
+  const int64_t e = a / n3;
+  const int l = (int)(a - e * n3);
+  const int loc[3] = {l % n, (l / n) % n, l / (n * n)};
+  const int64_t cell[3] = {e % b.ex, (e / b.ex) % b.ey, e / ((int64_t)b.ex * b.ey)};
+  boundary = false;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    g[d] = L.coord(d, cell[d], loc[d]);
+    if (loc[d] == 0 || loc[d] == b.N) boundary = true;
+  }
+}
+
+__device__ __forceinline__ bool lattice_masked(const Lattice& L, const int64_t g[3]) {
+  bool m = false;
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+    if (!L.per[d] && (g[d] == 0 || g[d] == (int64_t)L.counts[d] * L.N)) m = true;
+  return m;
+}
+
+__global__ void lattice_fields_kernel(BoxLat b, int64_t nodes, double* __restrict__ mask,
+                                      double* __restrict__ inv_mult,
+                                      uint8_t* __restrict__ mult8) {
+  const Lattice L = make_lattice(b);
+  for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < nodes;
+       a += (int64_t)gridDim.x * blockDim.x) {
+    int64_t g[3];
+    bool boundary;
+    node_coords(L, b, a, g, boundary);
+    int m = 1;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) m *= L.opts(d, g[d]).count;
+    if (mask) mask[a] = lattice_masked(L, g) ? 0.0 : 1.0;
+    if (inv_mult) inv_mult[a] = 1.0 / (double)m;
+    if (mult8) mult8[a] = (uint8_t)m;
+  }
+}
+
+__global__ void gs_box_kernel(BoxLat b, int64_t nodes, double* __restrict__ f, int apply_mask) {
+  const Lattice L = make_lattice(b);
+  const int n = b.N + 1;
+  const int64_t n3 = (int64_t)n * n * n;
+  for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < nodes;
+       a += (int64_t)gridDim.x * blockDim.x) {
+    int64_t g[3];
+    bool boundary;
+    node_coords(L, b, a, g, boundary);
+    if (!boundary) continue;  // element-interior: an unmasked singleton
+    int64_t el[8];
+    int li[8];
+    const int m = L.copies(g[0], g[1], g[2], el, li);
+    const bool masked = apply_mask && lattice_masked(L, g);
+    if (m == 1) {
+      if (masked) f[a] = __dmul_rn(f[a], 0.0);
+      continue;
+    }
+    if (el[0] * n3 + li[0] != a) continue;  // the group's first copy does the work
+    double s = 0.0;
+    for (int c = 0; c < m; ++c) s = __dadd_rn(s, f[el[c] * n3 + li[c]]);
+    const double v = masked ? __dmul_rn(s, 0.0) : s;
+    for (int c = 0; c < m; ++c) f[el[c] * n3 + li[c]] = v;
+  }
+}
+
+__global__ void check_rhs_box_kernel(BoxLat b, int64_t nodes, const double* __restrict__ f,
+                                     int* flag) {
+  const Lattice L = make_lattice(b);
+  const int n = b.N + 1;
+  const int64_t n3 = (int64_t)n * n * n;
+  bool bad = false;
+  for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < nodes;
+       a += (int64_t)gridDim.x * blockDim.x) {
+    int64_t g[3];
+    bool boundary;
+    node_coords(L, b, a, g, boundary);
+    if (!boundary) continue;
+    const double v = f[a];
+    if (lattice_masked(L, g) && v != 0.0) bad = true;
+    int64_t el[8];
+    int li[8];
+    const int m = L.copies(g[0], g[1], g[2], el, li);
+    for (int c = 0; c < m; ++c)
+      if (f[el[c] * n3 + li[c]] != v) bad = true;
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) *flag = 1;
+}
+
+unsigned grid_for(int64_t work) {
+  int64_t b = (work + 255) / 256;
+  if (b > 148 * 32) b = 148 * 32;
+  if (b < 1) b = 1;
+  return (unsigned)b;
+}
+
+BoxLat box_lat(const OpDev& op) {
+  return BoxLat{op.ex, op.ey, op.ez, {op.per[0], op.per[1], op.per[2]}, op.n - 1};
+}
+
+}  // namespace
+
+cudaError_t launch_geom_box(const double* corners, int64_t E, int n, const double* x,
+                            const double* w, double* G, double* bm, unsigned long long* bad,
+                            cudaStream_t s) {
+  GllParam q{};
+  for (int i = 0; i < n; ++i) {
+    q.x[i] = x[i];
+    q.w[i] = w[i];
+  }
+  geom_box_kernel<<<grid_for(E * n * n * n), 256, 0, s>>>(corners, E, n, q, G, bm, bad);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lattice_fields(const OpDev& op, double* mask, double* inv_mult,
+                                  uint8_t* mult8, cudaStream_t s) {
+  lattice_fields_kernel<<<grid_for(op.nodes), 256, 0, s>>>(box_lat(op), op.nodes, mask,
+                                                           inv_mult, mult8);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gs_box(const OpDev& op, double* f, bool apply_mask, cudaStream_t s) {
+  gs_box_kernel<<<grid_for(op.nodes), 256, 0, s>>>(box_lat(op), op.nodes, f,
+                                                   apply_mask ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_check_rhs_box(const OpDev& op, const double* f, int* flag, cudaStream_t s) {
+  check_rhs_box_kernel<<<grid_for(op.nodes), 256, 0, s>>>(box_lat(op), op.nodes, f, flag);
+  return cudaGetLastError();
+}
+
+}  // namespace sbx
