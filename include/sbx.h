@@ -109,6 +109,17 @@ typedef struct {
   int64_t global_count;         /* G                                              */
   const int64_t* group_offsets; /* G+1                                            */
   const int64_t* group_nodes;   /* E*n^3                                          */
+  /* Optional structured-box hint (HexMesh::ex/ey/ez, periodic, corners;
+   * mesh.hpp:14-33).  The reference's build_gather_scatter only accepts a
+   * structured box (gather.cpp:11-12), so a sembox caller always has these.
+   * When box[0] > 0 the context checks, on the device, that the map and mask
+   * ARE the box lattice's (and, with corners, that g1..g6 are the corners'
+   * trilinear metric, bitwise); if so it uses the lattice gather-scatter (no
+   * CSR is built) and the fused solver's trilinear K1 / lattice K2, else it
+   * falls back to the general path silently.  Zero-initialise to omit. */
+  int32_t box[3];               /* ex, ey, ez (0: no hint)                        */
+  int32_t periodic[3];
+  const double* corners;        /* [E][8][3] or NULL                              */
 } sbx_problem_desc;
 
 sbx_status sbx_ctx_create(const sbx_problem_desc* desc, int device, sbx_ctx** out);
@@ -132,6 +143,13 @@ void sbx_ctx_destroy(sbx_ctx* ctx);
 /* E, n, local nodes, G, device bytes */
 sbx_status sbx_ctx_info(const sbx_ctx* ctx, int64_t* elem_count, int32_t* n1d,
                         int64_t* nodes, int64_t* global_count, int64_t* device_bytes);
+
+/* Which fused paths a context runs (a problem built without the box hint,
+ * or whose hint did not verify, runs the general CSR / stored-geometry path). */
+#define SBX_FEAT_LATTICE_GS 0x1u /* gather-scatter on the box lattice, no CSR      */
+#define SBX_FEAT_BOX_K2 0x2u     /* lattice K2 (partner copies from the lattice)   */
+#define SBX_FEAT_TRILINEAR 0x4u  /* K1 forms the metric from the trilinear map     */
+sbx_status sbx_ctx_features(const sbx_ctx* ctx, uint32_t* features);
 
 /* copy context-owned arrays (reference layout) to host or device memory:
  * which = 0 mask, 1 inv_mult, 2 bm, 3..8 g1..g6, 9 deriv */

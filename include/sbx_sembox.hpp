@@ -23,6 +23,7 @@
 #include "sembox/field.hpp"
 #include "sembox/gather.hpp"
 #include "sembox/krylov.hpp"
+#include "sembox/mesh.hpp"
 #include "sembox/operators.hpp"
 
 namespace sbx_sembox {
@@ -45,7 +46,24 @@ inline void check(sbx_status st, int iteration = -1) {
 class Device {
  public:
   Device(const sembox::GeometricFactors& gf, const sembox::SpectralBasis& basis,
-         const sembox::GatherScatterMap& map, const sembox::Field* mask, int device = 0) {
+         const sembox::GatherScatterMap& map, const sembox::Field* mask, int device = 0)
+      : Device(nullptr, gf, basis, map, mask, device) {}
+
+  // With the mesh the map was built on (build_gather_scatter requires a
+  // structured box, gather.cpp:11-12): the context verifies on the device
+  // that map, mask and geometry are the box lattice's / the corners'
+  // trilinear metric and then runs the lattice gather-scatter and the
+  // trilinear-metric fused kernels -- the same kernels as a context built by
+  // sbx_ctx_create_box.
+  Device(const sembox::HexMesh& mesh, const sembox::GeometricFactors& gf,
+         const sembox::SpectralBasis& basis, const sembox::GatherScatterMap& map,
+         const sembox::Field* mask, int device = 0)
+      : Device(&mesh, gf, basis, map, mask, device) {}
+
+ private:
+  Device(const sembox::HexMesh* mesh, const sembox::GeometricFactors& gf,
+         const sembox::SpectralBasis& basis, const sembox::GatherScatterMap& map,
+         const sembox::Field* mask, int device) {
     sbx_problem_desc d{};
     d.elem_count = gf.elem_count;
     d.degree = basis.order;
@@ -57,10 +75,24 @@ class Device {
     d.global_count = map.global_count;
     d.group_offsets = map.group_offsets.data();
     d.group_nodes = map.group_nodes.data();
+    std::vector<double> corners;
+    if (mesh && mesh->structured() && mesh->elem_count == gf.elem_count) {
+      d.box[0] = mesh->ex;
+      d.box[1] = mesh->ey;
+      d.box[2] = mesh->ez;
+      for (int q = 0; q < 3; ++q) d.periodic[q] = mesh->periodic[q] ? 1 : 0;
+      corners.reserve((size_t)mesh->elem_count * 24);
+      for (const auto& el : mesh->corners)
+        for (const auto& p : el)
+          for (double v : p) corners.push_back(v);
+      d.corners = corners.data();
+    }
     check(sbx_ctx_create(&d, device, &ctx_));
     n1d_ = basis.n();
     elems_ = gf.elem_count;
   }
+
+ public:
   ~Device() { sbx_ctx_destroy(ctx_); }
   Device(const Device&) = delete;
   Device& operator=(const Device&) = delete;

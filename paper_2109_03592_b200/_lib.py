@@ -30,7 +30,8 @@ _u32 = C.c_uint32
 class ProblemDesc(C.Structure):
     _fields_ = [("elem_count", _i64), ("degree", _i32), ("deriv", _vp), ("g", _vp * 6),
                 ("bm", _vp), ("mask", _vp), ("global_count", _i64), ("group_offsets", _vp),
-                ("group_nodes", _vp)]
+                ("group_nodes", _vp), ("box", _i32 * 3), ("periodic", _i32 * 3),
+                ("corners", _vp)]
 
 
 class BoxDesc(C.Structure):
@@ -73,6 +74,7 @@ _sig("sbx_ctx_info", _i, _vp, C.POINTER(_i64), C.POINTER(_i32), C.POINTER(_i64),
      C.POINTER(_i64), C.POINTER(_i64))
 _sig("sbx_ctx_copy_array", _i, _vp, _i, _vp)
 _sig("sbx_ctx_set_stream", _i, _vp, _vp)
+_sig("sbx_ctx_features", _i, _vp, C.POINTER(_u32))
 _sig("sbx_axhelm", _i, _vp, _vp, _vp, _d, _d, _u32)
 _sig("sbx_axhelm_diagonal", _i, _vp, _d, _d, _i, _vp)
 _sig("sbx_gs_sum", _i, _vp, _vp)
@@ -96,6 +98,9 @@ _sig("sbx_debug_cg_k1", _i, _vp, _vp, _vp, _d, _d)
 FLAG_EXACT = 0x1
 FLAG_FLIP_T = 0x2
 FLAG_NO_MASK = 0x4
+FEAT_LATTICE_GS = 0x1
+FEAT_BOX_K2 = 0x2
+FEAT_TRILINEAR = 0x4
 MODE_EXACT = 0
 MODE_FAST = 1
 PRECOND_NONE = 0

@@ -301,7 +301,11 @@ class Context:
 
     @classmethod
     def from_problem(cls, gf: GeometricFactors, basis: SpectralBasis, gmap: GatherScatterMap,
-                     mask: Optional[np.ndarray], device: int = 0):
+                     mask: Optional[np.ndarray], device: int = 0, mesh: "HexMesh" = None):
+        """HelmholtzOperator's inputs as the reference builds them.  `mesh`
+        (optional) is the structured-box hint of sbx_problem_desc: the
+        context verifies the map/mask/geometry against it on the device and
+        then runs the lattice gather-scatter and the trilinear-metric K1."""
         if gf.n1d != basis.n() or gmap.n1d != basis.n() or gf.elem_count != gmap.elem_count:
             raise ContractViolation("HelmholtzOperator: grid/shape mismatch")
         keep = [np.ascontiguousarray(a, np.float64) for a in
@@ -320,6 +324,15 @@ class Context:
         d.global_count = gmap.global_count
         d.group_offsets = offs.ctypes.data
         d.group_nodes = nodes.ctypes.data
+        if mesh is not None and mesh.structured():
+            if mesh.elem_count != gf.elem_count:
+                raise ContractViolation("HelmholtzOperator: mesh / geometry size mismatch")
+            corners = np.ascontiguousarray(mesh.corners, np.float64)
+            keep.append(corners)
+            d.box[0], d.box[1], d.box[2] = mesh.ex, mesh.ey, mesh.ez
+            for q in range(3):
+                d.periodic[q] = int(bool(mesh.periodic[q]))
+            d.corners = corners.ctypes.data
         h = C.c_void_p()
         _check(lib.sbx_ctx_create(C.byref(d), device, C.byref(h)))
         return cls(h, device)
@@ -373,6 +386,14 @@ class Context:
         out = np.empty(count)
         _check(lib.sbx_ctx_copy_array(self._h, which, out.ctypes.data))
         return out
+
+    def features(self):
+        """{"lattice_gs", "box_k2", "trilinear"}: the fused paths this context runs."""
+        f = C.c_uint32()
+        _check(lib.sbx_ctx_features(self._h, C.byref(f)))
+        names = ((L.FEAT_LATTICE_GS, "lattice_gs"), (L.FEAT_BOX_K2, "box_k2"),
+                 (L.FEAT_TRILINEAR, "trilinear"))
+        return {nm for bit, nm in names if f.value & bit}
 
     def enable_timing(self, on=True):
         _check(lib.sbx_ctx_enable_timing(self._h, int(on)))

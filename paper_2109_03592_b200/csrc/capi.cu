@@ -282,6 +282,97 @@ sbx_status ensure_partials(sbx_ctx* c, int64_t count) {
   return SBX_OK;
 }
 
+// Trilinear-element data for the fused CG kernel's on-the-fly metrics: the
+// per-element map coefficients and the GLL nodes / weights.
+sbx_status upload_trilinear(sbx_ctx* c, int degree, const double* corners, int64_t E) {
+  std::vector<double> tl(E * 24);
+  trilinear_coeffs(E, corners, tl.data());
+  double* dtl = nullptr;
+  SBX_TRY(dupload(c, &dtl, tl.data(), E * 24));
+  c->op.tl = dtl;
+  SBX_TRY(sbx_gll_basis(degree, c->op.Xh, c->op.Wh, nullptr));
+  return SBX_OK;
+}
+
+
+// Structured-box hint of sbx_problem_desc: verify on the device that the
+// caller's map and mask are the lattice's (and the geometry the corners'
+// trilinear metric); if so switch the context to the lattice gather-scatter
+// (no CSR) and, with verified corners, the trilinear K1.  *lattice = false
+// (and nothing changed) when the hint is absent or does not match.
+sbx_status try_box_hint(sbx_ctx* c, const sbx_problem_desc* d, bool* lattice) {
+  *lattice = false;
+  const int64_t E = c->op.E, N = c->op.nodes;
+  if (d->box[0] <= 0 || d->box[1] <= 0 || d->box[2] <= 0 || !d->mask) return SBX_OK;
+  if ((int64_t)d->box[0] * d->box[1] * d->box[2] != E) return SBX_OK;
+  if (std::getenv("SBX_HOST_SETUP")) return SBX_OK;
+  OpDev probe = c->op;
+  probe.ex = d->box[0];
+  probe.ey = d->box[1];
+  probe.ez = d->box[2];
+  int64_t G = 1;
+  const int n = c->op.n;
+  for (int q = 0; q < 3; ++q) {
+    probe.per[q] = d->periodic[q] ? 1 : 0;
+    if (probe.per[q] && d->box[q] < 2) return SBX_OK;  // lattice gs needs 2 cells
+    const int64_t span = (int64_t)d->box[q] * (n - 1);
+    G *= probe.per[q] ? span : span + 1;
+  }
+  if (G != d->global_count || d->group_offsets[0] != 0 || d->group_offsets[G] != N)
+    return SBX_OK;
+  int* flag = reinterpret_cast<int*>(c->dcount) + 8;
+  SBX_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), c->stream));
+  {
+    int64_t *doff = nullptr, *didx = nullptr;
+    SBX_CUDA(cudaMalloc(&doff, sizeof(int64_t) * (size_t)(G + 1)));
+    SBX_CUDA(cudaMalloc(&didx, sizeof(int64_t) * (size_t)N));
+    SBX_CUDA(cudaMemcpyAsync(doff, d->group_offsets, sizeof(int64_t) * (size_t)(G + 1),
+                             cudaMemcpyHostToDevice, c->stream));
+    SBX_CUDA(cudaMemcpyAsync(didx, d->group_nodes, sizeof(int64_t) * (size_t)N,
+                             cudaMemcpyHostToDevice, c->stream));
+    SBX_CUDA(launch_validate_box(probe, G, doff, didx, c->op.mask, flag, c->stream));
+    SBX_CUDA(cudaStreamSynchronize(c->stream));
+    cudaFree(doff);
+    cudaFree(didx);
+  }
+  int bad = 0;
+  SBX_CUDA(cudaMemcpy(&bad, flag, sizeof(int), cudaMemcpyDeviceToHost));
+  if (bad) return SBX_OK;
+  // the map / mask are the lattice's: lattice gather-scatter, no CSR
+  double* im = nullptr;
+  uint8_t* m8 = nullptr;
+  SBX_TRY(dupload<double>(c, &im, nullptr, N));
+  SBX_TRY(dupload<uint8_t>(c, &m8, nullptr, N));
+  SBX_CUDA(launch_lattice_fields(probe, nullptr, im, m8, c->stream));
+  c->op = probe;
+  c->op.box = true;
+  c->op.lat = true;
+  c->op.inv_mult = im;
+  c->op.mult8 = m8;
+  c->op.nB = 0;
+  c->op.nBcopies = 0;
+  c->interior_clean = true;
+  *lattice = true;
+  // geometry from the corners (trilinear K1) only if it is bitwise the
+  // caller's g1..g6 / bm
+  if (d->corners) {
+    std::vector<double> x(n), w(n);
+    SBX_TRY(sbx_gll_basis(n - 1, x.data(), w.data(), nullptr));
+    double* dcr = nullptr;
+    SBX_CUDA(cudaMalloc(&dcr, sizeof(double) * (size_t)E * 24));
+    SBX_CUDA(cudaMemcpyAsync(dcr, d->corners, sizeof(double) * (size_t)E * 24,
+                             cudaMemcpyHostToDevice, c->stream));
+    SBX_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), c->stream));
+    SBX_CUDA(launch_validate_geom(dcr, E, n, x.data(), w.data(), c->op.G, c->op.bm, flag,
+                                  c->stream));
+    SBX_CUDA(cudaStreamSynchronize(c->stream));
+    cudaFree(dcr);
+    SBX_CUDA(cudaMemcpy(&bad, flag, sizeof(int), cudaMemcpyDeviceToHost));
+    if (!bad) SBX_TRY(upload_trilinear(c, n - 1, d->corners, E));
+  }
+  return SBX_OK;
+}
+
 // Upload the problem (reference layout host arrays) and re-lay it out.
 sbx_status ctx_upload(sbx_ctx* c, const sbx_problem_desc* d) {
   const int n = d->degree + 1;
@@ -321,7 +412,9 @@ sbx_status ctx_upload(sbx_ctx* c, const sbx_problem_desc* d) {
     c->op.mask = m;
     c->has_mask = true;
   }
-  SBX_TRY(build_boundary_csr(c, d->group_offsets, d->group_nodes, d->mask));
+  bool lattice = false;
+  SBX_TRY(try_box_hint(c, d, &lattice));
+  if (!lattice) SBX_TRY(build_boundary_csr(c, d->group_offsets, d->group_nodes, d->mask));
   SBX_TRY(ensure_partials(c, std::max<int64_t>(c->op.E, 4096)));
   c->cg.reset(new CgEngine());
   return SBX_OK;
@@ -582,18 +675,6 @@ sbx_status sbx_ctx_create(const sbx_problem_desc* desc, int device, sbx_ctx** ou
   return SBX_OK;
 }
 
-// Trilinear-element data for the fused CG kernel's on-the-fly metrics: the
-// per-element map coefficients and the GLL nodes / weights.
-sbx_status upload_trilinear(sbx_ctx* c, int degree, const double* corners, int64_t E) {
-  std::vector<double> tl(E * 24);
-  trilinear_coeffs(E, corners, tl.data());
-  double* dtl = nullptr;
-  SBX_TRY(dupload(c, &dtl, tl.data(), E * 24));
-  c->op.tl = dtl;
-  SBX_TRY(sbx_gll_basis(degree, c->op.Xh, c->op.Wh, nullptr));
-  return SBX_OK;
-}
-
 // Device-side setup of a structured box: geometry, mask
 // and multiplicities are built by kernels (setup_dev.cu) from the element
 // corners; the gather-scatter runs on the lattice, so no map is built or
@@ -783,6 +864,17 @@ sbx_status sbx_ctx_info(const sbx_ctx* c, int64_t* E, int32_t* n1d, int64_t* nod
   if (nodes) *nodes = c->op.nodes;
   if (G) *G = c->global_count;
   if (bytes) *bytes = c->device_bytes;
+  return SBX_OK;
+}
+
+sbx_status sbx_ctx_features(const sbx_ctx* c, uint32_t* f) {
+  SBX_TRY(check_ctx(c));
+  if (!f) {
+    set_error("sbx_ctx_features: null output");
+    return SBX_E_INVALID;
+  }
+  *f = (c->op.lat ? SBX_FEAT_LATTICE_GS : 0u) | (c->op.box ? SBX_FEAT_BOX_K2 : 0u) |
+       (c->op.tl ? SBX_FEAT_TRILINEAR : 0u);
   return SBX_OK;
 }
 

@@ -171,6 +171,15 @@ cudaError_t launch_lattice_fields(const OpDev& op, double* mask, double* inv_mul
                                   uint8_t* mult8, cudaStream_t s);
 cudaError_t launch_gs_box(const OpDev& op, double* f, bool apply_mask, cudaStream_t s);
 cudaError_t launch_check_rhs_box(const OpDev& op, const double* f, int* flag, cudaStream_t s);
+// *flag := 1 unless the caller's map (device int64 copies; may be null) and
+// mask (may be null) are the box lattice's of op (ex/ey/ez/per/n set)
+cudaError_t launch_validate_box(const OpDev& op, int64_t G, const int64_t* offsets,
+                                const int64_t* group_nodes, const double* mask, int* flag,
+                                cudaStream_t s);
+// *flag := 1 unless packed G (and bm, if given) equal the corners' metric bitwise
+cudaError_t launch_validate_geom(const double* corners, int64_t E, int n, const double* x,
+                                 const double* w, const double* G, const double* bm, int* flag,
+                                 cudaStream_t s);
 
 // ---- fused FAST CG (cg.cu) -------------------------------------------------
 // Whether the multi-GPU solver has a pipelined K1 (the halo leaves from its

@@ -165,6 +165,79 @@ __global__ void check_rhs_box_kernel(BoxLat b, int64_t nodes, const double* __re
   if (__syncthreads_or(bad) && threadIdx.x == 0) *flag = 1;
 }
 
+// The caller's map (group_offsets / group_nodes, gather.hpp:14-29) against
+// the lattice: one thread per group (= lattice point, gid order).
+__global__ void validate_map_kernel(BoxLat b, int64_t G, int64_t nodes,
+                                    const int64_t* __restrict__ off,
+                                    const int64_t* __restrict__ idx, int* flag) {
+  const Lattice L = make_lattice(b);
+  const int n = b.N + 1;
+  const int64_t n3 = (int64_t)n * n * n;
+  bool bad = false;
+  for (int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < G;
+       gid += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g0 = gid % L.gdim[0], g1 = (gid / L.gdim[0]) % L.gdim[1],
+                  g2 = gid / (L.gdim[0] * L.gdim[1]);
+    int64_t el[8];
+    int li[8];
+    const int m = L.copies(g0, g1, g2, el, li);
+    const int64_t lo = off[gid], hi = off[gid + 1];
+    if (hi - lo != m || lo < 0 || hi > nodes) {
+      bad = true;
+      continue;
+    }
+    for (int c = 0; c < m; ++c)
+      if (idx[lo + c] != el[c] * n3 + li[c]) bad = true;
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) *flag = 1;
+}
+
+__global__ void validate_mask_kernel(BoxLat b, int64_t nodes, const double* __restrict__ mask,
+                                     int* flag) {
+  const Lattice L = make_lattice(b);
+  bool bad = false;
+  for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < nodes;
+       a += (int64_t)gridDim.x * blockDim.x) {
+    int64_t g[3];
+    bool boundary;
+    node_coords(L, b, a, g, boundary);
+    const double want = lattice_masked(L, g) ? 0.0 : 1.0;
+    // bitwise (-0.0 is not the reference's 0.0)
+    if (__double_as_longlong(mask[a]) != __double_as_longlong(want)) bad = true;
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) *flag = 1;
+}
+
+// The caller's packed geometry against the corners' trilinear metric, bitwise.
+__global__ void validate_geom_kernel(const double* __restrict__ corners, int64_t E, int n,
+                                     GllParam q, const double* __restrict__ G,
+                                     const double* __restrict__ bm, int* flag) {
+  const int n3 = n * n * n;
+  const int64_t nodes = E * n3;
+  bool bad = false;
+  for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < nodes;
+       a += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = a / n3;
+    const int l = (int)(a - e * n3);
+    const int i = l % n, j = (l / n) % n, k = l / (n * n);
+    double cr[24];
+#pragma unroll
+    for (int c = 0; c < 24; ++c) cr[c] = __ldg(corners + e * 24 + c);
+    Metric m;
+    const double wq = q.w[i] * q.w[j] * q.w[k];
+    if (!node_metric(cr, q.x[i], q.x[j], q.x[k], wq, m)) {
+      bad = true;
+      continue;
+    }
+    const double* Ge = G + e * 6 * (int64_t)n3 + l;
+#pragma unroll
+    for (int c = 0; c < 6; ++c)
+      if (__double_as_longlong(Ge[c * n3]) != __double_as_longlong(m.g[c])) bad = true;
+    if (bm && __double_as_longlong(bm[a]) != __double_as_longlong(m.wdet)) bad = true;
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) *flag = 1;
+}
+
 unsigned grid_for(int64_t work) {
   int64_t b = (work + 255) / 256;
   if (b > 148 * 32) b = 148 * 32;
@@ -205,6 +278,29 @@ cudaError_t launch_gs_box(const OpDev& op, double* f, bool apply_mask, cudaStrea
 
 cudaError_t launch_check_rhs_box(const OpDev& op, const double* f, int* flag, cudaStream_t s) {
   check_rhs_box_kernel<<<grid_for(op.nodes), 256, 0, s>>>(box_lat(op), op.nodes, f, flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_validate_box(const OpDev& op, int64_t G, const int64_t* offsets,
+                                const int64_t* group_nodes, const double* mask, int* flag,
+                                cudaStream_t s) {
+  if (offsets && group_nodes)
+    validate_map_kernel<<<grid_for(G), 256, 0, s>>>(box_lat(op), G, op.nodes, offsets,
+                                                     group_nodes, flag);
+  if (mask) validate_mask_kernel<<<grid_for(op.nodes), 256, 0, s>>>(box_lat(op), op.nodes, mask,
+                                                                    flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_validate_geom(const double* corners, int64_t E, int n, const double* x,
+                                 const double* w, const double* G, const double* bm, int* flag,
+                                 cudaStream_t s) {
+  GllParam q{};
+  for (int i = 0; i < n; ++i) {
+    q.x[i] = x[i];
+    q.w[i] = w[i];
+  }
+  validate_geom_kernel<<<grid_for(E * n * n * n), 256, 0, s>>>(corners, E, n, q, G, bm, flag);
   return cudaGetLastError();
 }
 
