@@ -305,7 +305,7 @@ sbx_status try_box_hint(sbx_ctx* c, const sbx_problem_desc* d, bool* lattice) {
   const int64_t E = c->op.E, N = c->op.nodes;
   if (d->box[0] <= 0 || d->box[1] <= 0 || d->box[2] <= 0 || !d->mask) return SBX_OK;
   if ((int64_t)d->box[0] * d->box[1] * d->box[2] != E) return SBX_OK;
-  if (std::getenv("SBX_HOST_SETUP")) return SBX_OK;
+  if (std::getenv("SBX_HOST_SETUP") || N >= (int64_t)INT32_MAX) return SBX_OK;
   OpDev probe = c->op;
   probe.ex = d->box[0];
   probe.ey = d->box[1];

@@ -964,6 +964,74 @@ __global__ void cg_init_kernel(int64_t N, const double* __restrict__ b,
   if (threadIdx.x == 0) *counter = 0;
 }
 
+// Single-graph solve prologue (zero initial guess assumed, checked): r = b,
+// b'Wb and b'W(M b) in one pass that also scans x for nonzeros
+// (krylov.cpp:19-32); the last CTA sets up the device scalars exactly as the
+// host would (krylov.cpp:11-50) -- or flags why the general path is needed --
+// so the whole solve runs from one graph launch with one host sync.
+__global__ void cg_prologue_kernel(int64_t N, const double* __restrict__ b,
+                                   const double* __restrict__ x,
+                                   const double* __restrict__ dinv,
+                                   const double* __restrict__ wgt, double* __restrict__ r,
+                                   double* __restrict__ partials, CgScalars* __restrict__ sc,
+                                   const CgParams* __restrict__ prm, double* __restrict__ hist,
+                                   const int* __restrict__ rhs_flag) {
+  __shared__ double red[32];
+  __shared__ bool is_last;
+  double s0 = 0.0, s1 = 0.0;
+  bool nz = false;
+  for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < N;
+       a += (int64_t)gridDim.x * blockDim.x) {
+    const double bv = b[a], wv = wgt[a];
+    r[a] = bv;
+    const double di = dinv ? dinv[a] : 1.0;
+    s0 += bv * bv * wv;
+    s1 += bv * (bv * di) * wv;
+    nz |= (x[a] != 0.0);  // NaN counts as nonzero, as in the reference
+  }
+  if (__syncthreads_or(nz) && threadIdx.x == 0) atomicOr(&sc->pre, kPreNonzeroX);
+  const double v0 = cta_sum(s0, red);
+  if (threadIdx.x == 0) partials[2 * (int64_t)blockIdx.x] = v0;
+  const double v1 = cta_sum(s1, red);
+  if (threadIdx.x == 0) partials[2 * (int64_t)blockIdx.x + 1] = v1;
+  if (!last_block(&sc->counter[2], &is_last)) return;
+  const double bb = reduce_partials(partials, gridDim.x, 2, 0, red);
+  const double bmb = reduce_partials(partials, gridDim.x, 2, 1, red);
+  if (threadIdx.x != 0) return;
+  sc->counter[2] = 0;
+  int pre = *(volatile int*)&sc->pre;
+  if (*rhs_flag) pre |= kPreRhsBad;
+  if (!(pre & (kPreNonzeroX | kPreRhsBad)) && bb == 0.0) pre |= kPreZeroRhs;
+  sc->pre = pre;
+  sc->it = 0;
+  sc->max_it = prm->max_it;
+  sc->tol = prm->tol;
+  sc->first = 1;
+  sc->status = 0;
+  sc->err_it = -1;
+  sc->nranks = 1;
+  sc->converged = 0;
+  sc->alpha = sc->alpha_prev = sc->beta = sc->pq = 0.0;
+  if (pre) {
+    sc->done = 1;
+    return;
+  }
+  // r = b (zero guess): rr = b'Wb, rz = b'W(M b)
+  const double bnorm = sqrt(bb), rnorm = sqrt(bb);
+  const double rel0 = rnorm / bnorm;
+  const double relp0 = bmb > 0.0 ? sqrt(fmax(bmb, 0.0) / bmb) : 0.0;
+  sc->rz = bmb;
+  sc->rr = bb;
+  sc->bnorm = bnorm;
+  sc->bmb = bmb;
+  sc->rel = rel0;
+  sc->relp = relp0;
+  hist[0] = rel0;
+  const bool conv0 = rel0 <= prm->tol && relp0 <= prm->tol;
+  sc->converged = conv0 ? 1 : 0;
+  sc->done = (conv0 || prm->max_it <= 0) ? 1 : 0;
+}
+
 // Continuity + mask check of the right-hand side on the boundary groups: the
 // fused p'Ap identity needs b (hence r, z, p) equal on all copies and zero
 // on masked copies.  flag := 1 on violation.
@@ -1352,6 +1420,16 @@ cudaError_t launch_dist_allreduce(const DistDev& D, int phase, const double* in,
     }                                                                       \
   } while (0)
 
+// CG iterations per WHILE body (SBX_CG_UNROLL, default 4)
+int cg_unroll() {
+  static const int u = [] {
+    const char* v = std::getenv("SBX_CG_UNROLL");
+    const int x = v ? std::atoi(v) : 4;
+    return x < 1 ? 1 : (x > 16 ? 16 : x);
+  }();
+  return u;
+}
+
 CgEngine::~CgEngine() {
   if (exec_) cudaGraphExecDestroy(exec_);
   if (graph_) cudaGraphDestroy(graph_);
@@ -1363,6 +1441,10 @@ CgEngine::~CgEngine() {
   cudaFree(hist_);
   cudaFree(init_);
   cudaFree(flag_);
+  cudaFree(prm_);
+  if (hprm_) cudaFreeHost(hprm_);
+  if (sexec_) cudaGraphExecDestroy(sexec_);
+  if (sgraph_) cudaGraphDestroy(sgraph_);
   if (hsc_) cudaFreeHost(hsc_);
 }
 
@@ -1379,6 +1461,7 @@ int CgEngine::ensure(const CgRun& run) {
     op_ = run.op;
     nodes_ = op.nodes;
     have_graph_ = false;
+    have_sgraph_ = false;
   }
   const int64_t need = 4 * std::max<int64_t>(std::max(k1_blocks(op), k2_blocks(op)), 2048);
   if (partials_len_ < need) {
@@ -1386,6 +1469,7 @@ int CgEngine::ensure(const CgRun& run) {
     CG_CUDA(cudaMalloc(&partials_, sizeof(double) * need));
     partials_len_ = need;
     have_graph_ = false;
+    have_sgraph_ = false;
   }
   if (!sc_) {
     CG_CUDA(cudaMalloc(&sc_, sizeof(CgScalars)));
@@ -1393,12 +1477,15 @@ int CgEngine::ensure(const CgRun& run) {
     CG_CUDA(cudaMallocHost(&hsc_, sizeof(CgScalars)));
     CG_CUDA(cudaMalloc(&init_, 8 * sizeof(double)));
     CG_CUDA(cudaMalloc(&flag_, 4 * sizeof(int)));
+    CG_CUDA(cudaMalloc(&prm_, sizeof(CgParams)));
+    CG_CUDA(cudaMallocHost(&hprm_, sizeof(CgParams)));
   }
   if (hist_len_ < (int64_t)run.max_it + 1) {
     cudaFree(hist_);
     hist_len_ = (int64_t)run.max_it + 1;
     CG_CUDA(cudaMalloc(&hist_, sizeof(double) * hist_len_));
     have_graph_ = false;
+    have_sgraph_ = false;
   }
   return SBX_OK;
 }
@@ -1426,11 +1513,7 @@ int CgEngine::build_graph(const CgRun& run) {
   // solve is done (sc->done), and the last K2 that ran sets the condition, so
   // the loop still stops on the exact iteration; the while-node's per-body
   // overhead is paid once per kUnroll iterations.
-  static const int kUnroll = [] {
-    const char* v = std::getenv("SBX_CG_UNROLL");
-    const int u = v ? std::atoi(v) : 4;
-    return u < 1 ? 1 : (u > 16 ? 16 : u);
-  }();
+  const int kUnroll = cg_unroll();
   cudaError_t e1 = cudaSuccess, e2 = cudaSuccess;
   for (int u = 0; u < kUnroll && e1 == cudaSuccess && e2 == cudaSuccess; ++u) {
     e1 = k1(op, r_, run.dinv, p_, run.x, w_, run.h1, run.h2, sc_, partials_, run.stream);
@@ -1453,9 +1536,113 @@ int CgEngine::build_graph(const CgRun& run) {
   CG_CUDA(e2);
   CG_CUDA(e3);
   CG_CUDA(cudaGraphInstantiate(&exec_, graph_, 0));
-  key_ = Key{run.op, run.x, run.dinv, run.h1, run.h2, hist_, run.stream};
+  key_ = Key{run.op, run.x, run.dinv, run.h1, run.h2, hist_, run.stream, nullptr};
   have_graph_ = true;
   return SBX_OK;
+}
+
+// The whole single-GPU solve as one graph: [continuity check of b] ->
+// prologue (r = b, initial sums, zero-guess scan, device scalars) -> WHILE
+// {kUnroll x (K1, K2)} -> x += alpha p of the last iteration.
+int CgEngine::build_solve_graph(const CgRun& run) {
+  const OpDev& op = *run.op;
+  const int64_t N = op.nodes;
+  cudaStream_t s = run.stream;
+  if (sexec_) cudaGraphExecDestroy(sexec_);
+  if (sgraph_) cudaGraphDestroy(sgraph_);
+  sexec_ = nullptr;
+  sgraph_ = nullptr;
+  have_sgraph_ = false;
+  CG_CUDA(cudaGraphCreate(&sgraph_, 0));
+  // prologue
+  cudaGraph_t pre = nullptr;
+  CG_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+  cudaMemsetAsync(flag_, 0, sizeof(int), s);
+  cudaMemsetAsync(&sc_->pre, 0, sizeof(int32_t), s);
+  if (op.lat)
+    launch_check_rhs_box(op, run.b, flag_, s);
+  else if (op.nB > 0)
+    cg_check_rhs_kernel<<<(unsigned)((op.nB + 255) / 256), 256, 0, s>>>(op.b_off, op.b_idx,
+                                                                        op.nB, run.b, flag_);
+  {
+    int64_t blocks = std::min<int64_t>((N + 1023) / 1024, 1184);
+    if (blocks < 1) blocks = 1;
+    cg_prologue_kernel<<<(unsigned)blocks, 256, 0, s>>>(N, run.b, run.x, run.dinv, op.inv_mult,
+                                                        r_, partials_, sc_, prm_, hist_, flag_);
+  }
+  const cudaError_t ep = cudaGetLastError();
+  CG_CUDA(cudaStreamEndCapture(s, &pre));
+  CG_CUDA(ep);
+  cudaGraphNode_t npre, nloop, npost;
+  CG_CUDA(cudaGraphAddChildGraphNode(&npre, sgraph_, nullptr, 0, pre));
+  cudaGraphDestroy(pre);
+  // the iteration loop
+  cudaGraphConditionalHandle handle;
+  CG_CUDA(cudaGraphConditionalHandleCreate(&handle, sgraph_, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams params = {};
+  params.type = cudaGraphNodeTypeConditional;
+  params.conditional.handle = handle;
+  params.conditional.type = cudaGraphCondTypeWhile;
+  params.conditional.size = 1;
+  CG_CUDA(cudaGraphAddNode(&nloop, sgraph_, &npre, 1, &params));
+  cudaGraph_t body = params.conditional.phGraph_out[0];
+  CG_CUDA(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0,
+                                        cudaStreamCaptureModeRelaxed));
+  const int unroll = cg_unroll();
+  cudaError_t e1 = cudaSuccess, e2 = cudaSuccess;
+  for (int u = 0; u < unroll && e1 == cudaSuccess && e2 == cudaSuccess; ++u) {
+    e1 = k1(op, r_, run.dinv, p_, run.x, w_, run.h1, run.h2, sc_, partials_, s);
+    e2 = k2(op, w_, r_, run.dinv, sc_, partials_, hist_, hist_len_, handle, 1, s);
+  }
+  cudaGraph_t captured = nullptr;
+  const cudaError_t e3 = cudaStreamEndCapture(s, &captured);
+  CG_CUDA(e1);
+  CG_CUDA(e2);
+  CG_CUDA(e3);
+  // x += alpha p of the last completed iteration
+  cudaGraph_t post = nullptr;
+  CG_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+  cg_finish_kernel<<<(unsigned)std::min<int64_t>((N + 255) / 256, 148 * 16), 256, 0, s>>>(
+      N, p_, run.x, sc_);
+  const cudaError_t ef = cudaGetLastError();
+  CG_CUDA(cudaStreamEndCapture(s, &post));
+  CG_CUDA(ef);
+  CG_CUDA(cudaGraphAddChildGraphNode(&npost, sgraph_, &nloop, 1, post));
+  cudaGraphDestroy(post);
+  CG_CUDA(cudaGraphInstantiate(&sexec_, sgraph_, 0));
+  skey_ = Key{run.op, run.x, run.dinv, run.h1, run.h2, hist_, run.stream, run.b};
+  have_sgraph_ = true;
+  return SBX_OK;
+}
+
+int CgEngine::solve_graph(const CgRun& run, sbx_pcg_result* res, bool* general) {
+  cudaStream_t s = run.stream;
+  *general = false;
+  const Key k{run.op, run.x, run.dinv, run.h1, run.h2, hist_, run.stream, run.b};
+  if (!have_sgraph_ || !(k == skey_)) {
+    const int rc = build_solve_graph(run);
+    if (rc != SBX_OK) return rc;
+  }
+  hprm_->tol = run.tol;
+  hprm_->max_it = run.max_it;
+  CG_CUDA(cudaMemcpyAsync(prm_, hprm_, sizeof(CgParams), cudaMemcpyHostToDevice, s));
+  CG_CUDA(cudaGraphLaunch(sexec_, s));
+  CG_CUDA(cudaMemcpyAsync(hsc_, sc_, sizeof(CgScalars), cudaMemcpyDeviceToHost, s));
+  CG_CUDA(cudaStreamSynchronize(s));
+  const int pre = hsc_->pre;
+  if (pre & kPreRhsBad) return kCgFallback;  // x untouched: the EXACT path runs
+  if (pre & kPreNonzeroX) {
+    *general = true;  // x untouched: r = b - A x0 on the general path
+    return SBX_OK;
+  }
+  res->history_length = 0;
+  if (pre & kPreZeroRhs) {
+    CG_CUDA(cudaMemsetAsync(run.x, 0, sizeof(double) * run.op->nodes, s));
+    CG_CUDA(cudaStreamSynchronize(s));
+    res->converged = 1;
+    return SBX_OK;
+  }
+  return collect(run, res);
 }
 
 int CgEngine::run_timed_loop(const CgRun& run) {
@@ -1499,6 +1686,13 @@ int CgEngine::solve(const CgRun& run, sbx_pcg_result* res) {
   cudaStream_t s = run.stream;
   const int64_t N = op.nodes;
   const DistDev* D = run.dist;
+  if (!D && !run.timing) {
+    // one graph launch and one host sync for the whole solve; the general
+    // path below only when the device prologue says so (nonzero guess)
+    bool general = false;
+    const int rc = solve_graph(run, res, &general);
+    if (!general) return rc;
+  }
   // right-hand side must be continuous and masked for the fused p'Ap
   // (checked on this rank's shared groups; cross-rank continuity is the
   // caller's contract in the distributed case)
@@ -1602,7 +1796,7 @@ int CgEngine::solve(const CgRun& run, sbx_pcg_result* res) {
     if (run.timing) {
       if (run_timed_loop(run) != SBX_OK) return SBX_E_CUDA;
     } else {
-      const Key k{run.op, run.x, run.dinv, run.h1, run.h2, hist_, run.stream};
+      const Key k{run.op, run.x, run.dinv, run.h1, run.h2, hist_, run.stream, nullptr};
       if (!have_graph_ || !(k == key_)) {
         const int rc = build_graph(run);
         if (rc != SBX_OK) return rc;
@@ -1615,6 +1809,11 @@ int CgEngine::solve(const CgRun& run, sbx_pcg_result* res) {
   }
   CG_CUDA(cudaMemcpyAsync(hsc_, sc_, sizeof(CgScalars), cudaMemcpyDeviceToHost, s));
   CG_CUDA(cudaStreamSynchronize(s));
+  return collect(run, res);
+}
+
+// Results of a finished solve from the scalars already copied to hsc_.
+int CgEngine::collect(const CgRun& run, sbx_pcg_result* res) {
   const CgScalars& o = *hsc_;
   res->iterations = o.it;
   res->converged = o.converged;

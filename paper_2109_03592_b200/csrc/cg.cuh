@@ -48,6 +48,9 @@ class CgEngine {
  private:
   int ensure(const CgRun& run);
   int build_graph(const CgRun& run);
+  int build_solve_graph(const CgRun& run);
+  int solve_graph(const CgRun& run, sbx_pcg_result* res, bool* general);
+  int collect(const CgRun& run, sbx_pcg_result* res);
   int run_timed_loop(const CgRun& run);
 
   const OpDev* op_ = nullptr;
@@ -63,6 +66,12 @@ class CgEngine {
   int64_t hist_len_ = 0;
   double* init_ = nullptr;    // device init sums [4]
   int* flag_ = nullptr;       // device continuity flag
+  CgParams* prm_ = nullptr;   // device solve parameters
+  CgParams* hprm_ = nullptr;  // pinned
+  // the single-graph solve (prologue + loop + finish), cached like graph_
+  cudaGraph_t sgraph_ = nullptr;
+  cudaGraphExec_t sexec_ = nullptr;
+  bool have_sgraph_ = false;
   // graph cache
   cudaGraph_t graph_ = nullptr;
   cudaGraphExec_t exec_ = nullptr;
@@ -73,11 +82,12 @@ class CgEngine {
     double h1, h2;
     const void* hist;
     cudaStream_t stream;
+    const void* b;
     bool operator==(const Key& o) const {
       return op == o.op && x == o.x && dinv == o.dinv && h1 == o.h1 && h2 == o.h2 &&
-             hist == o.hist && stream == o.stream;
+             hist == o.hist && stream == o.stream && b == o.b;
     }
-  } key_{};
+  } key_{}, skey_{};
   bool have_graph_ = false;
   // per-kernel timing (timing mode)
   double t_ax_ms_ = 0, t_upd_ms_ = 0;

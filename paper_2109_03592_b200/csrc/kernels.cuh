@@ -73,6 +73,19 @@ struct CgScalars {
   int32_t nranks;   // > 1: distributed (rank-local partials, exchange kernels)
   uint32_t counter[4];  // last-block-done tickets
   double pq_loc, rz_loc, rr_loc;  // this rank's partials (distributed)
+  // single-graph solve: what the device prologue found (kPre* bits)
+  int32_t pre;
+  int32_t pad_;
+};
+// CgScalars::pre
+constexpr int kPreNonzeroX = 1;  // x0 != 0: r = b - A x0 needs the general path
+constexpr int kPreRhsBad = 2;    // b not continuous / not masked: EXACT fallback
+constexpr int kPreZeroRhs = 4;   // b'Wb == 0: x = 0, converged (krylov.cpp:11-16)
+// solve parameters read by the device prologue (H2D before each graph launch)
+struct CgParams {
+  double tol;
+  int32_t max_it;
+  int32_t pad_;
 };
 
 // ---- multi-GPU peer windows ------------------------------------------------

@@ -116,51 +116,154 @@ __global__ void lattice_fields_kernel(BoxLat b, int64_t nodes, double* __restric
   }
 }
 
-__global__ void gs_box_kernel(BoxLat b, int64_t nodes, double* __restrict__ f, int apply_mask) {
-  const Lattice L = make_lattice(b);
-  const int n = b.N + 1;
-  const int64_t n3 = (int64_t)n * n * n;
-  for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < nodes;
-       a += (int64_t)gridDim.x * blockDim.x) {
-    int64_t g[3];
-    bool boundary;
-    node_coords(L, b, a, g, boundary);
-    if (!boundary) continue;  // element-interior: an unmasked singleton
-    int64_t el[8];
-    int li[8];
-    const int m = L.copies(g[0], g[1], g[2], el, li);
-    const bool masked = apply_mask && lattice_masked(L, g);
-    if (m == 1) {
-      if (masked) f[a] = __dmul_rn(f[a], 0.0);
-      continue;
+// ---- per-solve lattice kernels: 32-bit, one thread per element column -----
+// (thread = (element e, column (i, j)); only the column's element-boundary
+// nodes do work: all k when i or j is on a face, else k = 0 and k = N)
+
+// copies of one lattice direction (32-bit Lattice::opts)
+struct Ax32 {
+  int cnt;
+  int cell[2];
+  int loc[2];
+};
+
+__device__ __forceinline__ Ax32 axis32(int g, int count, int N, bool per) {
+  Ax32 o;
+  const int q = g / N, r = g - q * N;
+  if (r != 0) {
+    o.cnt = 1;
+    o.cell[0] = q;
+    o.loc[0] = r;
+    return o;
+  }
+  o.cnt = 0;
+  if (per) {
+    o.cell[0] = q;
+    o.loc[0] = 0;
+    o.cell[1] = (q - 1 + count) % count;
+    o.loc[1] = N;
+    o.cnt = 2;
+  } else {
+    if (g > 0) {
+      o.cell[o.cnt] = q - 1;
+      o.loc[o.cnt++] = N;
     }
-    if (el[0] * n3 + li[0] != a) continue;  // the group's first copy does the work
-    double s = 0.0;
-    for (int c = 0; c < m; ++c) s = __dadd_rn(s, f[el[c] * n3 + li[c]]);
-    const double v = masked ? __dmul_rn(s, 0.0) : s;
-    for (int c = 0; c < m; ++c) f[el[c] * n3 + li[c]] = v;
+    if (q < count) {
+      o.cell[o.cnt] = q;
+      o.loc[o.cnt++] = 0;
+    }
+  }
+  return o;
+}
+
+struct Col32 {
+  int e, i, j, cx, cy, cz;
+};
+
+__device__ __forceinline__ Col32 col_of(const BoxLat& b, int n, int col) {
+  Col32 c;
+  const int nn = n * n;
+  c.e = col / nn;
+  const int ij = col - c.e * nn;
+  c.j = ij / n;
+  c.i = ij - c.j * n;
+  const int exy = b.ex * b.ey;
+  c.cz = c.e / exy;
+  const int rxy = c.e - c.cz * exy;
+  c.cy = rxy / b.ex;
+  c.cx = rxy - c.cy * b.ex;
+  return c;
+}
+
+// lattice coordinate along d of local index loc in cell c (periodic wrap)
+__device__ __forceinline__ int gcoord(int c, int loc, int count, int N, bool per) {
+  const int g = c * N + loc;
+  return (per && g == count * N) ? 0 : g;
+}
+
+// All copies of node (col, k) in ascending local index (the reference's
+// group order): returns the count; idx[] = e * n^3 + local index.
+__device__ __forceinline__ int copies32(const BoxLat& b, int n, const Col32& c, int k,
+                                        int (&idx)[8], bool& masked) {
+  const int N = n - 1, n3 = n * n * n;
+  const int gx = gcoord(c.cx, c.i, b.ex, N, b.per[0]);
+  const int gy = gcoord(c.cy, c.j, b.ey, N, b.per[1]);
+  const int gz = gcoord(c.cz, k, b.ez, N, b.per[2]);
+  masked = (!b.per[0] && (gx == 0 || gx == b.ex * N)) ||
+           (!b.per[1] && (gy == 0 || gy == b.ey * N)) ||
+           (!b.per[2] && (gz == 0 || gz == b.ez * N));
+  const Ax32 ox = axis32(gx, b.ex, N, b.per[0]);
+  const Ax32 oy = axis32(gy, b.ey, N, b.per[1]);
+  const Ax32 oz = axis32(gz, b.ez, N, b.per[2]);
+  int m = 0;
+  for (int z = 0; z < oz.cnt; ++z)
+    for (int y = 0; y < oy.cnt; ++y)
+      for (int x = 0; x < ox.cnt; ++x) {
+        const int e = ox.cell[x] + b.ex * (oy.cell[y] + b.ey * oz.cell[z]);
+        idx[m++] = e * n3 + (oz.loc[z] * n + oy.loc[y]) * n + ox.loc[x];
+      }
+  for (int x = 1; x < m; ++x)  // <= 8 copies; already sorted unless a periodic wrap
+    for (int y = x; y > 0 && idx[y - 1] > idx[y]; --y) {
+      const int t = idx[y - 1];
+      idx[y - 1] = idx[y];
+      idx[y] = t;
+    }
+  return m;
+}
+
+__global__ void gs_box_kernel(BoxLat b, int n, int cols, double* __restrict__ f,
+                              int apply_mask) {
+  const int N = n - 1, n3 = n * n * n;
+  for (int col = blockIdx.x * blockDim.x + threadIdx.x; col < cols;
+       col += gridDim.x * blockDim.x) {
+    const Col32 c = col_of(b, n, col);
+    const bool face = c.i == 0 || c.i == N || c.j == 0 || c.j == N;
+    for (int k = 0; k < n; k += (face || k == N) ? 1 : N) {
+      const int a = c.e * n3 + (k * n + c.j) * n + c.i;
+      int idx[8];
+      bool masked;
+      const int m = copies32(b, n, c, k, idx, masked);
+      masked = masked && apply_mask;
+      if (m == 1) {
+        if (masked) f[a] = __dmul_rn(f[a], 0.0);
+        continue;
+      }
+      if (idx[0] != a) continue;  // the group's first copy does the work
+      double sum = 0.0;
+      for (int q = 0; q < m; ++q) sum = __dadd_rn(sum, f[idx[q]]);
+      const double v = masked ? __dmul_rn(sum, 0.0) : sum;
+      for (int q = 0; q < m; ++q) f[idx[q]] = v;
+    }
   }
 }
 
-__global__ void check_rhs_box_kernel(BoxLat b, int64_t nodes, const double* __restrict__ f,
+// Continuity: every copy equals its face neighbours' copies (the copies of a
+// node are connected by face steps, so pairwise face equality is equality of
+// all copies); masked copies are zero.
+__global__ void check_rhs_box_kernel(BoxLat b, int n, int cols, const double* __restrict__ f,
                                      int* flag) {
-  const Lattice L = make_lattice(b);
-  const int n = b.N + 1;
-  const int64_t n3 = (int64_t)n * n * n;
+  const int N = n - 1, n3 = n * n * n;
   bool bad = false;
-  for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < nodes;
-       a += (int64_t)gridDim.x * blockDim.x) {
-    int64_t g[3];
-    bool boundary;
-    node_coords(L, b, a, g, boundary);
-    if (!boundary) continue;
-    const double v = f[a];
-    if (lattice_masked(L, g) && v != 0.0) bad = true;
-    int64_t el[8];
-    int li[8];
-    const int m = L.copies(g[0], g[1], g[2], el, li);
-    for (int c = 0; c < m; ++c)
-      if (f[el[c] * n3 + li[c]] != v) bad = true;
+  for (int col = blockIdx.x * blockDim.x + threadIdx.x; col < cols;
+       col += gridDim.x * blockDim.x) {
+    const Col32 c = col_of(b, n, col);
+    const bool face = c.i == 0 || c.i == N || c.j == 0 || c.j == N;
+    // partner across the +x / +y / +z face (loc == N), with the wrap
+    const int ex1 = (c.cx + 1 < b.ex) ? 1 : (b.per[0] ? 1 - b.ex : 0);
+    const int ey1 = (c.cy + 1 < b.ey) ? b.ex : (b.per[1] ? (1 - b.ey) * b.ex : 0);
+    const int exy = b.ex * b.ey;
+    const int ez1 = (c.cz + 1 < b.ez) ? exy : (b.per[2] ? (1 - b.ez) * exy : 0);
+    const bool mx = !b.per[0] && ((c.cx == 0 && c.i == 0) || (c.cx == b.ex - 1 && c.i == N));
+    const bool my = !b.per[1] && ((c.cy == 0 && c.j == 0) || (c.cy == b.ey - 1 && c.j == N));
+    for (int k = 0; k < n; k += (face || k == N) ? 1 : N) {
+      const int l = (k * n + c.j) * n + c.i;
+      const double v = f[c.e * n3 + l];
+      const bool mz = !b.per[2] && ((c.cz == 0 && k == 0) || (c.cz == b.ez - 1 && k == N));
+      if ((mx || my || mz) && v != 0.0) bad = true;
+      if (c.i == N && ex1 != 0 && f[(c.e + ex1) * n3 + l - N] != v) bad = true;
+      if (c.j == N && ey1 != 0 && f[(c.e + ey1) * n3 + l - N * n] != v) bad = true;
+      if (k == N && ez1 != 0 && f[(c.e + ez1) * n3 + l - N * n * n] != v) bad = true;
+    }
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) *flag = 1;
 }
@@ -271,13 +374,14 @@ cudaError_t launch_lattice_fields(const OpDev& op, double* mask, double* inv_mul
 }
 
 cudaError_t launch_gs_box(const OpDev& op, double* f, bool apply_mask, cudaStream_t s) {
-  gs_box_kernel<<<grid_for(op.nodes), 256, 0, s>>>(box_lat(op), op.nodes, f,
-                                                   apply_mask ? 1 : 0);
+  const int cols = (int)(op.E * op.n * op.n);
+  gs_box_kernel<<<grid_for(cols), 256, 0, s>>>(box_lat(op), op.n, cols, f, apply_mask ? 1 : 0);
   return cudaGetLastError();
 }
 
 cudaError_t launch_check_rhs_box(const OpDev& op, const double* f, int* flag, cudaStream_t s) {
-  check_rhs_box_kernel<<<grid_for(op.nodes), 256, 0, s>>>(box_lat(op), op.nodes, f, flag);
+  const int cols = (int)(op.E * op.n * op.n);
+  check_rhs_box_kernel<<<grid_for(cols), 256, 0, s>>>(box_lat(op), op.n, cols, f, flag);
   return cudaGetLastError();
 }
 

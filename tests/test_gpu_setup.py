@@ -112,3 +112,54 @@ def test_device_setup_time_bench_mesh(cuda):
     assert c.nodes == 64 ** 3 * 512
     c.close()
     assert dt < 3.0
+
+
+def test_problem_with_box_hint_runs_the_box_kernels(cuda):
+    """sbx_problem_desc's structured-box hint (the reference's HexMesh): the
+    reference-layout map / mask / geometry are verified on the device, then
+    the context runs exactly the kernels of Context.box -- identical bits."""
+    torch = cuda
+    dims, N, deform = (5, 4, 3), 7, 0.05
+    mesh, basis, gf, gmap, mask = host_problem(dims, N, (False,) * 3, deform)
+    hinted = sb.Context.from_problem(gf, basis, gmap, mask, mesh=mesh)
+    plain = sb.Context.from_problem(gf, basis, gmap, mask)
+    box = sb.Context.box(*dims, N, deform=deform)
+    assert hinted.features() == {"lattice_gs", "box_k2", "trilinear"}
+    assert plain.features() == set()
+    assert box.features() == {"lattice_gs", "box_k2", "trilinear"}
+    P = O.Problem(*dims, N, corners=mesh.corners)
+    b = torch.from_numpy(P.rhs_random_continuous(77)).cuda()
+    xs = []
+    for ctx in (hinted, box, plain):
+        x = torch.zeros_like(b)
+        r = sb.pcg(sb.HelmholtzOperator(ctx), b, x, sb.KrylovConfig(1e-9, 2000))
+        xs.append((r.iterations, x))
+    assert xs[0][0] == xs[1][0] == xs[2][0]
+    assert torch.equal(xs[0][1], xs[1][1])
+    assert float((xs[0][1] - xs[2][1]).norm() / xs[2][1].norm()) <= 1e-10
+
+
+def test_box_hint_that_does_not_match_is_ignored(cuda):
+    dims, N, deform = (3, 3, 2), 5, 0.05
+    mesh, basis, gf, gmap, mask = host_problem(dims, N, (False,) * 3, deform)
+    # geometry that is not the corners' trilinear metric: lattice gs, stored G
+    g2 = sb.GeometricFactors(gf.elem_count, gf.n1d, gf.g1 * 1.5, gf.g2, gf.g3, gf.g4, gf.g5,
+                             gf.g6, gf.bm, gf.jac)
+    ctx = sb.Context.from_problem(g2, basis, gmap, mask, mesh=mesh)
+    assert ctx.features() == {"lattice_gs", "box_k2"}
+    # a mask that is not the box's Dirichlet mask: the general CSR path
+    m2 = mask.copy()
+    m2[7] = 1.0 - m2[7]
+    ctx2 = sb.Context.from_problem(gf, basis, gmap, m2, mesh=mesh)
+    assert ctx2.features() == set()
+    u = O.fill_uniform(3, ctx2.nodes)
+    P = O.Problem(*dims, N, corners=mesh.corners)
+    want = P.axhelm(u, 1.0, 0.0)
+    P.gs_sum_inplace(want)
+    got = np.empty_like(u)
+    sb.HelmholtzOperator(ctx2, use_mask=False, exact=True).apply(u, got)
+    assert np.array_equal(got, want)
+    # a mesh hint of the wrong shape: ignored
+    mesh3 = sb.build_box_mesh(3, 2, 3, deform=deform)
+    ctx3 = sb.Context.from_problem(gf, basis, gmap, mask, mesh=mesh3)
+    assert ctx3.features() == set()
