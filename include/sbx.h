@@ -220,6 +220,41 @@ void sbx_pcg_config_default(sbx_pcg_config* cfg);
 sbx_status sbx_pcg(sbx_ctx* ctx, const double* b, double* x, const sbx_pcg_config* cfg,
                    sbx_pcg_result* result);
 
+/* ------------------------------------ consistent-Poisson pressure path ---
+ * The P_N / P_N-2 pressure operator E = Div M^-1 QQ^T Grad of the paper's
+ * splitting scheme.  Pressure fields: E * m^3 doubles,
+ * m = N-1 GL points per direction (GridTag::pressure, field.hpp:13-16), same
+ * element-major x-fastest order.  Needs N >= 3 and a context with the element
+ * corners (sbx_ctx_create_box, or sbx_ctx_create with a verified box hint);
+ * flags: SBX_FLAG_EXACT = the reference's evaluation order (bitwise equal,
+ * the geometry from the corners as build_pressure_geometry forms it); default
+ * FAST (fused kernels, the GL metric from the trilinear map on the fly, the
+ * reference's results to rounding). */
+
+/* build_pressure_basis (basis.cpp:114-145): nodes[m], weights[m],
+ * interp_v2p[m*(N+1)] (row-major l_j(gl_i)). */
+sbx_status sbx_pressure_basis(int degree, double* nodes, double* weights, double* interp_v2p);
+/* pressure nodes E*m^3 and m */
+sbx_status sbx_pressure_info(sbx_ctx* ctx, int64_t* pressure_nodes, int32_t* m1d);
+/* gradient_from_pressure (operators.hpp:78-80, operators.cpp:365-410) */
+sbx_status sbx_gradient_from_pressure(sbx_ctx* ctx, const double* p, double* gx, double* gy,
+                                      double* gz, uint32_t flags);
+/* divergence_to_pressure (operators.hpp:73-75, operators.cpp:327-363) */
+sbx_status sbx_divergence_to_pressure(sbx_ctx* ctx, const double* ux, const double* uy,
+                                      const double* uz, double* out, uint32_t flags);
+/* FlowSolver::apply_pressure_operator (stepper.cpp:240-248): Div (mask/gs(bm)) gs Grad p */
+sbx_status sbx_pressure_apply(sbx_ctx* ctx, const double* p, double* out, uint32_t flags);
+/* FlowSolver::pressure_operator_diagonal (stepper.cpp:250-275) */
+sbx_status sbx_pressure_diagonal(sbx_ctx* ctx, double* diag, uint32_t flags);
+/* the pressure solve of FlowSolver::solve_pressure_update (stepper.cpp:326-347):
+ * pcg with apply_pressure_operator, field_dot (plain) and pressure_precond
+ * (stepper.cpp:277-308: Jacobi on the diagonal or none, each followed by the
+ * mean deflation).  cfg->precond JACOBI or NONE; cfg->mode EXACT (the
+ * reference's residual history bit for bit) or FAST; h1/h2 unused.
+ * b must already have its mean removed (stepper.cpp:313-324). */
+sbx_status sbx_pressure_pcg(sbx_ctx* ctx, const double* b, double* x, const sbx_pcg_config* cfg,
+                            sbx_pcg_result* result);
+
 /* -------------------------------------------------------- multi-GPU ------ */
 /* One process per GPU; elements of a structured box are partitioned by
  * partition_rcb (mesh.cpp:168-226).  Shared nodes on rank boundaries are

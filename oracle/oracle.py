@@ -144,6 +144,13 @@ def _ref():
         L.ref_pcg.argtypes = [_P, C.c_double, C.c_double, C.c_int, _dp, _dp, C.c_double,
                               C.c_int, _i64p, _dp, _dp, C.c_int64, _i64p]
         L.ref_partition_rcb.argtypes = [_P, C.c_int, _i32p]
+        L.ref_pressure_setup.argtypes = [_P]
+        L.ref_pressure_copy.argtypes = [_P, C.c_int, _dp]
+        L.ref_gradient_from_pressure.argtypes = [_P, _dp, _dp, _dp, _dp]
+        L.ref_divergence_to_pressure.argtypes = [_P, _dp, _dp, _dp, _dp]
+        L.ref_pressure_apply.argtypes = [_P, _dp, _dp]
+        L.ref_pressure_pcg.argtypes = [_P, C.c_int, _dp, _dp, C.c_double, C.c_int, _i64p, _dp,
+                                       _dp, C.c_int64, _i64p]
         L.ref_bench_prepare.argtypes = [_P, C.c_double, C.c_double, _dp]
         L.ref_bench_solve.argtypes = [_P, C.c_int, _i64p, _dp]
         L.ref_dense_helmholtz_element.argtypes = [_P, C.c_int, C.c_double, C.c_double, _dp]
@@ -356,6 +363,76 @@ class Problem:
                                 h2, pc, b, x, tol, max_iterations, info, res, hist, cap, hlen)
         return PcgOut(int(info[0]), bool(info[1]), float(res[0]), float(res[1]),
                       hist[: min(int(hlen[0]), cap)].copy(), x, int(rc), int(info[2]))
+
+    # -- consistent-Poisson pressure path (reference backend only) ---------
+    # stepper.cpp:59-84 setup, operators.cpp:327-410, stepper.cpp:240-348
+    def pressure_setup(self):
+        assert self.backend == "ref"
+        rc = _ref().ref_pressure_setup(self._h)
+        if rc:
+            raise OracleError(rc, _ref().ref_last_error().decode())
+        self.m = self.degree - 1
+        self.pnodes_count = self.E * self.m ** 3
+
+    def pressure_array(self, which):
+        """0 GL nodes, 1 GL weights, 2 interp_v2p, 3 wdetj, 4 drdx, 5 inv_bdiag,
+        6 the Jacobi diagonal (pressure_operator_diagonal)."""
+        m, n = self.m, self.n
+        count = [m, m, m * n, self.pnodes_count, 9 * self.pnodes_count, self.nodes_count,
+                 self.pnodes_count][which]
+        out = np.empty(count)
+        _ref().ref_pressure_copy(self._h, which, out)
+        return out
+
+    def gradient_from_pressure(self, p):
+        g = [np.empty(self.nodes_count) for _ in range(3)]
+        rc = _ref().ref_gradient_from_pressure(self._h, np.ascontiguousarray(p, np.float64), *g)
+        if rc:
+            raise OracleError(rc, _ref().ref_last_error().decode())
+        return g
+
+    def divergence_to_pressure(self, ux, uy, uz):
+        out = np.empty(self.pnodes_count)
+        rc = _ref().ref_divergence_to_pressure(self._h, *[np.ascontiguousarray(u, np.float64)
+                                                          for u in (ux, uy, uz)], out)
+        if rc:
+            raise OracleError(rc, _ref().ref_last_error().decode())
+        return out
+
+    def pressure_apply(self, p):
+        out = np.empty(self.pnodes_count)
+        rc = _ref().ref_pressure_apply(self._h, np.ascontiguousarray(p, np.float64), out)
+        if rc:
+            raise OracleError(rc, _ref().ref_last_error().decode())
+        return out
+
+    def pressure_pcg(self, b, precond="jacobi", tol=1e-6, max_iterations=500, x0=None):
+        pc = {"none": 0, None: 0, "jacobi": 1}[precond]
+        b = np.ascontiguousarray(b, np.float64)
+        x = np.zeros(self.pnodes_count) if x0 is None else np.array(x0, np.float64)
+        info = np.zeros(3, np.int64)
+        res = np.zeros(2)
+        cap = max_iterations + 1
+        hist = np.zeros(cap)
+        hlen = np.zeros(1, np.int64)
+        rc = _ref().ref_pressure_pcg(self._h, pc, b, x, tol, max_iterations, info, res, hist,
+                                     cap, hlen)
+        return PcgOut(int(info[0]), bool(info[1]), float(res[0]), float(res[1]),
+                      hist[: min(int(hlen[0]), cap)].copy(), x, int(rc), int(info[2]))
+
+    def pressure_rhs(self, seed=5):
+        """A pressure right-hand side as solve_pressure_update forms it
+        (stepper.cpp:311-324): the divergence of a random continuous, masked
+        velocity field, mean removed."""
+        u = []
+        for d in range(3):
+            f = fill_uniform(seed + d, self.nodes_count)
+            self.gs_sum_inplace(f)
+            f *= self.inv_mult * self.mask
+            u.append(f)
+        rhs = self.divergence_to_pressure(*u)
+        rhs -= rhs.sum() / rhs.size
+        return rhs
 
     # -- benchmark session (reference backend only) ------------------------
     def bench_prepare(self, b, h1=1.0, h2=0.0):

@@ -26,6 +26,8 @@
 #include <random>
 #include <string>
 
+#include <algorithm>
+
 #include "sembox/basis.hpp"
 #include "sembox/errors.hpp"
 #include "sembox/field.hpp"
@@ -62,7 +64,52 @@ struct Problem {
   // and Jacobi diagonal kept here so a timed step is the pcg call itself
   Field bench_b, bench_x, bench_diag;
   double bench_h1 = 0.0, bench_h2 = 0.0;
+  // consistent-Poisson pressure path (ref_pressure_setup)
+  bool has_p = false;
+  PressureBasis pb;
+  PressureGeometry pg;
+  Field inv_bdiag, pdiag;
 };
+
+// FlowSolver::apply_pressure_operator (stepper.cpp:240-248), restated with the
+// reference's own operators (stepper.cpp itself cannot be linked: it needs
+// schwarz.cpp / Eigen3).
+void pressure_apply(const Problem& p, const Field& x, Field& out) {
+  VectorField g = gradient_from_pressure(x, p.pg, p.basis, p.pb);
+  for (int d = 0; d < 3; ++d) {
+    gs_sum_inplace(p.map, g[d]);
+    field_pointwise_mul(p.inv_bdiag, g[d]);
+  }
+  out = divergence_to_pressure(g[0], g[1], g[2], p.pg, p.basis, p.pb);
+}
+
+// FlowSolver::pressure_operator_diagonal (stepper.cpp:250-275), restated.
+Field pressure_diagonal(const Problem& p) {
+  const int m = p.pb.m(), n = p.basis.n();
+  const int mm = m * m * m, nn = n * n * n;
+  Field diag(GridTag::pressure, p.mesh.elem_count, m);
+  parallel_for(p.mesh.elem_count, [&](std::int64_t e) {
+    PressureGeometry pge;
+    pge.elem_count = 1;
+    pge.m1d = m;
+    pge.wdetj.assign(p.pg.wdetj.begin() + e * mm, p.pg.wdetj.begin() + (e + 1) * mm);
+    pge.drdx.assign(p.pg.drdx.begin() + e * mm * 9, p.pg.drdx.begin() + (e + 1) * mm * 9);
+    Field unit(GridTag::pressure, 1, m);
+    for (int q = 0; q < mm; ++q) {
+      std::fill(unit.v.begin(), unit.v.end(), 0.0);
+      unit.v[q] = 1.0;
+      const VectorField g = gradient_from_pressure(unit, pge, p.basis, p.pb);
+      double s = 0.0;
+      for (int d = 0; d < 3; ++d)
+        for (int a = 0; a < nn; ++a) {
+          const double v = g[d].v[a];
+          s += v * v * p.inv_bdiag.v[e * nn + a];
+        }
+      diag.v[e * mm + q] = s;
+    }
+  });
+  return diag;
+}
 
 template <typename F>
 int guarded(F&& f) {
@@ -338,6 +385,133 @@ int ref_bench_solve(void* h, int iters, std::int64_t* info, double* res) {
     info[1] = r.converged ? 1 : 0;
     res[0] = r.rel_residual;
     res[1] = r.rel_residual_precond;
+  });
+}
+
+// ---- consistent-Poisson pressure path ----------------
+// Setup as FlowSolver's constructor does it (stepper.cpp:59-84, 110-111):
+// the GL pressure basis and geometry, the inverse assembled (masked) mass.
+int ref_pressure_setup(void* h) {
+  auto* p = static_cast<Problem*>(h);
+  return guarded([&] {
+    p->pb = build_pressure_basis(p->basis.order);
+    p->pg = build_pressure_geometry(p->mesh, p->pb);
+    Field bdiag(GridTag::velocity, p->mesh.elem_count, p->basis.n());
+    std::copy(p->gf.bm.begin(), p->gf.bm.end(), bdiag.v.begin());
+    gs_sum_inplace(p->map, bdiag);
+    p->inv_bdiag = Field(GridTag::velocity, p->mesh.elem_count, p->basis.n());
+    for (std::int64_t a = 0; a < bdiag.size(); ++a)
+      p->inv_bdiag.v[a] = p->mask.v[a] / bdiag.v[a];
+    p->pdiag = pressure_diagonal(*p);
+    p->has_p = true;
+  });
+}
+
+// which: 0 GL nodes [m], 1 GL weights [m], 2 interp_v2p [m*n], 3 wdetj
+// [E m^3], 4 drdx [E m^3 9], 5 inv_bdiag [E n^3], 6 the Jacobi diagonal [E m^3]
+void ref_pressure_copy(void* h, int which, double* out) {
+  auto* p = static_cast<Problem*>(h);
+  const std::vector<double>* src = which == 0   ? &p->pb.nodes
+                                   : which == 1 ? &p->pb.weights
+                                   : which == 2 ? &p->pb.interp_v2p
+                                   : which == 3 ? &p->pg.wdetj
+                                   : which == 4 ? &p->pg.drdx
+                                   : which == 5 ? &p->inv_bdiag.v
+                                                : &p->pdiag.v;
+  std::memcpy(out, src->data(), src->size() * sizeof(double));
+}
+
+int ref_gradient_from_pressure(void* h, const double* pin, double* gx, double* gy,
+                               double* gz) {
+  auto* p = static_cast<Problem*>(h);
+  return guarded([&] {
+    Field f(GridTag::pressure, p->mesh.elem_count, p->pb.m());
+    std::memcpy(f.v.data(), pin, f.v.size() * sizeof(double));
+    const VectorField g = gradient_from_pressure(f, p->pg, p->basis, p->pb);
+    unwrap(g[0], gx);
+    unwrap(g[1], gy);
+    unwrap(g[2], gz);
+  });
+}
+
+int ref_divergence_to_pressure(void* h, const double* ux, const double* uy, const double* uz,
+                               double* out) {
+  auto* p = static_cast<Problem*>(h);
+  return guarded([&] {
+    const Field d = divergence_to_pressure(wrap(*p, ux), wrap(*p, uy), wrap(*p, uz), p->pg,
+                                           p->basis, p->pb);
+    unwrap(d, out);
+  });
+}
+
+int ref_pressure_apply(void* h, const double* x, double* out) {
+  auto* p = static_cast<Problem*>(h);
+  return guarded([&] {
+    Field f(GridTag::pressure, p->mesh.elem_count, p->pb.m()), o;
+    std::memcpy(f.v.data(), x, f.v.size() * sizeof(double));
+    pressure_apply(*p, f, o);
+    unwrap(o, out);
+  });
+}
+
+// The pressure solve of FlowSolver::solve_pressure_update (stepper.cpp:310-348)
+// on a given (already deflated) right-hand side and initial guess: the
+// reference pcg with apply_pressure_operator, the preconditioner of
+// pressure_precond (stepper.cpp:277-308: Jacobi on pressure_operator_diagonal
+// or none, each followed by the mean deflation) and the plain field_dot.
+int ref_pressure_pcg(void* h, int precond, const double* b, double* x, double tol,
+                     int max_iterations, std::int64_t* info, double* res, double* history,
+                     std::int64_t hist_cap, std::int64_t* hist_len) {
+  auto* p = static_cast<Problem*>(h);
+  info[0] = 0;
+  info[1] = 0;
+  info[2] = -1;
+  *hist_len = 0;
+  return guarded([&] {
+    const int m = p->pb.m();
+    const auto deflate = [](Field& z) {
+      double mean = 0.0;
+      for (double v : z.v) mean += v;
+      mean /= static_cast<double>(z.size());
+      for (double& v : z.v) v -= mean;
+    };
+    PrecondFn pre;
+    if (precond == 1) {
+      const Field* diag = &p->pdiag;
+      pre = [diag, deflate](const Field& r, Field& z) {
+        if (!z.same_shape(r)) z = Field(r.tag, r.elem_count, r.n1d);
+        for (std::int64_t a = 0; a < r.size(); ++a) z.v[a] = r.v[a] / diag->v[a];
+        deflate(z);
+      };
+    } else {
+      pre = [deflate](const Field& r, Field& z) {
+        field_copy(r, z);
+        deflate(z);
+      };
+    }
+    const ApplyFn apply_e = [p](const Field& in, Field& out) { pressure_apply(*p, in, out); };
+    KrylovConfig cfg;
+    cfg.tolerance = tol;
+    cfg.max_iterations = max_iterations;
+    Field bf(GridTag::pressure, p->mesh.elem_count, m), xf(GridTag::pressure,
+                                                          p->mesh.elem_count, m);
+    std::memcpy(bf.v.data(), b, bf.v.size() * sizeof(double));
+    std::memcpy(xf.v.data(), x, xf.v.size() * sizeof(double));
+    try {
+      const PcgResult r = pcg(apply_e, bf, pre, field_dot, cfg, xf);
+      info[0] = r.iterations;
+      info[1] = r.converged ? 1 : 0;
+      res[0] = r.rel_residual;
+      res[1] = r.rel_residual_precond;
+      const std::int64_t n =
+          std::min<std::int64_t>(hist_cap, static_cast<std::int64_t>(r.residual_history.size()));
+      for (std::int64_t i = 0; i < n; ++i) history[i] = r.residual_history[i];
+      *hist_len = static_cast<std::int64_t>(r.residual_history.size());
+    } catch (const SolverError& e) {
+      info[2] = e.iteration;
+      throw;
+    }
+    unwrap(xf, x);
   });
 }
 

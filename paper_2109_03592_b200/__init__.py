@@ -17,6 +17,8 @@ from .api import (  # noqa: F401
     KrylovConfig,
     MeshError,
     PcgResult,
+    PressureBasis,
+    PressureOperator,
     SemboxError,
     SolverError,
     SpectralBasis,
@@ -28,12 +30,16 @@ from .api import (  # noqa: F401
     build_gather_scatter,
     build_geometric_factors,
     build_gll_basis,
+    build_pressure_basis,
+    divergence_to_pressure,
+    gradient_from_pressure,
     field_dot,
     field_dot_weighted,
     gs_sum,
     gs_sum_inplace,
     partition_rcb,
     pcg,
+    pcg_pressure,
 )
 
 __version__ = "0.1.0"

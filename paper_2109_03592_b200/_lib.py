@@ -94,6 +94,13 @@ _sig("sbx_ctx_local_elements", _i, _vp, _vp)
 _sig("sbx_ctx_enable_timing", _i, _vp, _i)
 _sig("sbx_ctx_kernel_time", _i, _vp, C.c_char_p, C.POINTER(_d), C.POINTER(_i64))
 _sig("sbx_debug_cg_k1", _i, _vp, _vp, _vp, _d, _d)
+_sig("sbx_pressure_basis", _i, _i, _vp, _vp, _vp)
+_sig("sbx_pressure_info", _i, _vp, C.POINTER(_i64), C.POINTER(_i32))
+_sig("sbx_gradient_from_pressure", _i, _vp, _vp, _vp, _vp, _vp, _u32)
+_sig("sbx_divergence_to_pressure", _i, _vp, _vp, _vp, _vp, _vp, _u32)
+_sig("sbx_pressure_apply", _i, _vp, _vp, _vp, _u32)
+_sig("sbx_pressure_diagonal", _i, _vp, _vp, _u32)
+_sig("sbx_pressure_pcg", _i, _vp, _vp, _vp, C.POINTER(PcgConfig), C.POINTER(PcgResultC))
 
 FLAG_EXACT = 0x1
 FLAG_FLIP_T = 0x2

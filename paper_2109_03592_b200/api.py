@@ -524,3 +524,126 @@ def pcg(op: HelmholtzOperator, b, x, cfg: KrylovConfig = KrylovConfig(),
     if hist is not None:
         out.residual_history = hist[: min(r.history_length, hist.size)].tolist()
     return out
+
+
+# ------------------------------------------------ pressure (P_N / P_N-2) ----
+@dataclass
+class PressureBasis:
+    """basis.hpp:21-35"""
+
+    order: int            # N-2
+    velocity_order: int   # N
+    nodes: np.ndarray     # N-1 GL points
+    weights: np.ndarray
+    interp_v2p: np.ndarray  # (N-1) x (N+1) row-major
+
+    def m(self):
+        return self.order + 1
+
+    def nv(self):
+        return self.velocity_order + 1
+
+
+def build_pressure_basis(velocity_degree: int) -> PressureBasis:
+    """basis.hpp:46 / basis.cpp:114-145"""
+    m = max(velocity_degree - 1, 1)
+    nodes, weights = np.zeros(m), np.zeros(m)
+    interp = np.zeros(m * (velocity_degree + 1))
+    _check(lib.sbx_pressure_basis(velocity_degree, nodes.ctypes.data, weights.ctypes.data,
+                                  interp.ctypes.data))
+    return PressureBasis(velocity_degree - 2, velocity_degree, nodes, weights, interp)
+
+
+def _pnodes(ctx: Context):
+    n, m = C.c_int64(), C.c_int32()
+    _check(lib.sbx_pressure_info(ctx.handle, C.byref(n), C.byref(m)))
+    return n.value
+
+
+def _pshape(ctx, *fields):
+    N = _pnodes(ctx)
+    for f in fields:
+        size = f.size if isinstance(f, np.ndarray) else f.numel()
+        if size != N:
+            raise ContractViolation("pressure field does not match the pressure grid")
+    return N
+
+
+def gradient_from_pressure(p, ctx: Context, exact=False):
+    """operators.hpp:78-80 / operators.cpp:365-410 -> [gx, gy, gz] (velocity grid);
+    exact = the reference's evaluation order (bitwise)."""
+    p = _f64(p)
+    _pshape(ctx, p)
+    if isinstance(p, np.ndarray):
+        out = [np.empty(ctx.nodes) for _ in range(3)]
+    else:
+        out = [p.new_empty(ctx.nodes) for _ in range(3)]
+    _check(lib.sbx_gradient_from_pressure(ctx.handle, _ptr(p), *[_ptr(o) for o in out],
+                                          L.FLAG_EXACT if exact else 0))
+    return out
+
+
+def divergence_to_pressure(ux, uy, uz, ctx: Context, exact=False):
+    """operators.hpp:73-75 / operators.cpp:327-363 (pressure grid)."""
+    u = [_f64(v) for v in (ux, uy, uz)]
+    ctx._shape_check(*u)
+    N = _pnodes(ctx)
+    out = np.empty(N) if isinstance(u[0], np.ndarray) else u[0].new_empty(N)
+    _check(lib.sbx_divergence_to_pressure(ctx.handle, *[_ptr(v) for v in u], _ptr(out),
+                                          L.FLAG_EXACT if exact else 0))
+    return out
+
+
+class PressureOperator:
+    """FlowSolver::apply_pressure_operator / pressure_operator_diagonal
+    (stepper.cpp:240-275): E p = Div (mask / gs(bm)) gs Grad p."""
+
+    def __init__(self, ctx: Context, exact: bool = False):
+        self.ctx = ctx
+        self.exact = exact
+        self.nodes = _pnodes(ctx)
+
+    def apply(self, p, out):
+        p = _f64(p)
+        _pshape(self.ctx, p, out)
+        _check(lib.sbx_pressure_apply(self.ctx.handle, _ptr(p), _ptr(out),
+                                      L.FLAG_EXACT if self.exact else 0))
+        return out
+
+    __call__ = apply
+
+    def diagonal(self):
+        out = np.empty(self.nodes)
+        _check(lib.sbx_pressure_diagonal(self.ctx.handle, out.ctypes.data,
+                                         L.FLAG_EXACT if self.exact else 0))
+        return out
+
+
+def pcg_pressure(op: PressureOperator, b, x, cfg: KrylovConfig = KrylovConfig(),
+                 precond: Optional[str] = "jacobi", history=True, mode: str = "fast") -> PcgResult:
+    """The pressure solve of FlowSolver::solve_pressure_update
+    (stepper.cpp:326-347): pcg with the pressure operator, the plain field_dot
+    and pressure_precond (Jacobi or none, each with the mean deflation).  b
+    must have its mean removed (stepper.cpp:313-324); x is the initial guess
+    in / solution out.  mode "exact" reproduces the reference bit for bit,
+    "fast" is the fused device loop."""
+    b = _f64(b)
+    _pshape(op.ctx, b, x)
+    c = L.PcgConfig()
+    lib.sbx_pcg_config_default(C.byref(c))
+    c.tolerance = cfg.tolerance
+    c.max_iterations = cfg.max_iterations
+    c.precond = L.PRECOND_JACOBI if precond == "jacobi" else L.PRECOND_NONE
+    c.mode = L.MODE_EXACT if mode == "exact" else L.MODE_FAST
+    hist = None
+    if history:
+        hist = np.zeros(max(cfg.max_iterations, 0) + 1)
+        c.history = hist.ctypes.data
+        c.history_capacity = hist.size
+    r = L.PcgResultC()
+    rc = lib.sbx_pressure_pcg(op.ctx.handle, _ptr(b), _ptr(x), C.byref(c), C.byref(r))
+    _check(rc, r.error_iteration)
+    out = PcgResult(r.iterations, r.rel_residual, r.rel_residual_precond, bool(r.converged))
+    if hist is not None:
+        out.residual_history = hist[: min(r.history_length, hist.size)].tolist()
+    return out

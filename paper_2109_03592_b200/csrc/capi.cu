@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "cg.cuh"
+#include "pressure.cuh"
 #include "kernels.cuh"
 #include "sbx_internal.h"
 
@@ -70,6 +71,8 @@ struct sbx_ctx {
   double diag_h1 = NAN, diag_h2 = NAN;
   // fast CG
   std::unique_ptr<CgEngine> cg;
+  // consistent-Poisson pressure operator (built on first use)
+  std::unique_ptr<PressureEngine> pe;
   // distributed (filled by sbx_ctx_create_box_dist)
   std::vector<int64_t> local_elements;
   bool dist = false;
@@ -290,6 +293,9 @@ sbx_status upload_trilinear(sbx_ctx* c, int degree, const double* corners, int64
   double* dtl = nullptr;
   SBX_TRY(dupload(c, &dtl, tl.data(), E * 24));
   c->op.tl = dtl;
+  double* dcr = nullptr;  // the corners themselves (EXACT pressure geometry)
+  SBX_TRY(dupload(c, &dcr, corners, E * 24));
+  c->op.corners = dcr;
   SBX_TRY(sbx_gll_basis(degree, c->op.Xh, c->op.Wh, nullptr));
   return SBX_OK;
 }
@@ -847,6 +853,7 @@ void sbx_ctx_destroy(sbx_ctx* c) {
     }
   }
   c->cg.reset();
+  c->pe.reset();
   for (void* p : c->peer_windows) cudaIpcCloseMemHandle(p);
   if (c->window) cudaFree(c->window);
   for (void* p : c->allocs) cudaFree(p);
@@ -1154,6 +1161,184 @@ sbx_status sbx_debug_cg_k1(sbx_ctx* c, const double* u, double* w, double h1, do
     SBX_CUDA(cudaMemcpyAsync(w, dw, sizeof(double) * (size_t)c->op.nodes, cudaMemcpyDeviceToHost,
                              c->stream));
   return finish(c);
+}
+
+// ---- consistent-Poisson pressure operator ------------
+sbx_status sbx_pressure_basis(int degree, double* nodes, double* weights, double* interp) {
+  const int rc = pressure_basis(degree, nodes, weights, interp);
+  if (rc)
+    set_error("build_pressure_basis: velocity degree must be >= 3 (no interior pressure grid "
+              "below that), got " + std::to_string(degree));
+  return (sbx_status)rc;
+}
+
+static sbx_status pressure_enter(sbx_ctx* c) {
+  SBX_TRY(check_ctx(c));
+  if (c->dist) {
+    set_error("pressure operator: single-process contexts only");
+    return SBX_E_CONFIG;
+  }
+  SBX_TRY(enter(c));
+  if (!c->pe) c->pe.reset(new PressureEngine());
+  const int rc = c->pe->setup(c->op, c->stream);
+  if (rc != SBX_OK) {
+    set_error(c->pe->error());
+    return (sbx_status)rc;
+  }
+  return SBX_OK;
+}
+
+sbx_status sbx_pressure_info(sbx_ctx* c, int64_t* pnodes, int32_t* m1d) {
+  SBX_TRY(pressure_enter(c));
+  if (pnodes) *pnodes = c->pe->pnodes();
+  if (m1d) *m1d = c->pe->m1d();
+  return finish(c);
+}
+
+// pressure-grid vectors share the velocity-size work buffers (E m^3 < E n^3)
+static sbx_status stage_p(sbx_ctx* c, const double* p, int64_t count, int slot,
+                          const double** out) {
+  if (is_device_ptr(p)) {
+    *out = p;
+    return SBX_OK;
+  }
+  double* w = nullptr;
+  SBX_TRY(work(c, slot, &w));
+  SBX_CUDA(cudaMemcpyAsync(w, p, sizeof(double) * (size_t)count, cudaMemcpyHostToDevice,
+                           c->stream));
+  *out = w;
+  return SBX_OK;
+}
+
+sbx_status sbx_gradient_from_pressure(sbx_ctx* c, const double* p, double* gx, double* gy,
+                                      double* gz, uint32_t flags) {
+  if (!p || !gx || !gy || !gz) {
+    set_error("sbx_gradient_from_pressure: null field");
+    return SBX_E_INVALID;
+  }
+  SBX_TRY(pressure_enter(c));
+  const double* dp = nullptr;
+  SBX_TRY(stage_p(c, p, c->pe->pnodes(), 0, &dp));
+  double* outs[3] = {gx, gy, gz};
+  double* d[3];
+  for (int q = 0; q < 3; ++q) {
+    d[q] = outs[q];
+    if (!is_device_ptr(outs[q])) SBX_TRY(work(c, 1 + q, &d[q]));
+  }
+  const int grc = (flags & SBX_FLAG_EXACT) ? c->pe->grad_exact(dp, d, c->stream)
+                                            : c->pe->grad(dp, d, c->stream);
+  if (grc != SBX_OK) {
+    set_error(c->pe->error());
+    return (sbx_status)grc;
+  }
+  for (int q = 0; q < 3; ++q)
+    if (d[q] != outs[q])
+      SBX_CUDA(cudaMemcpyAsync(outs[q], d[q], sizeof(double) * (size_t)c->op.nodes,
+                               cudaMemcpyDeviceToHost, c->stream));
+  return finish(c);
+}
+
+sbx_status sbx_divergence_to_pressure(sbx_ctx* c, const double* ux, const double* uy,
+                                      const double* uz, double* out, uint32_t flags) {
+  if (!ux || !uy || !uz || !out) {
+    set_error("sbx_divergence_to_pressure: null field");
+    return SBX_E_INVALID;
+  }
+  SBX_TRY(pressure_enter(c));
+  const double* in[3] = {ux, uy, uz};
+  const double* d[3];
+  for (int q = 0; q < 3; ++q) SBX_TRY(stage_in(c, in[q], q, &d[q]));
+  const bool odev = is_device_ptr(out);
+  double* o = out;
+  if (!odev) SBX_TRY(work(c, 3, &o));
+  const int drc = (flags & SBX_FLAG_EXACT) ? c->pe->div_exact(d, o, c->stream)
+                                            : c->pe->div(d, o, c->stream);
+  if (drc != SBX_OK) {
+    set_error(c->pe->error());
+    return (sbx_status)drc;
+  }
+  if (!odev)
+    SBX_CUDA(cudaMemcpyAsync(out, o, sizeof(double) * (size_t)c->pe->pnodes(),
+                             cudaMemcpyDeviceToHost, c->stream));
+  return finish(c);
+}
+
+sbx_status sbx_pressure_apply(sbx_ctx* c, const double* p, double* out, uint32_t flags) {
+  if (!p || !out) {
+    set_error("sbx_pressure_apply: null field");
+    return SBX_E_INVALID;
+  }
+  SBX_TRY(pressure_enter(c));
+  const double* dp = nullptr;
+  SBX_TRY(stage_p(c, p, c->pe->pnodes(), 0, &dp));
+  const bool odev = is_device_ptr(out);
+  double* o = out;
+  if (!odev) SBX_TRY(work(c, 1, &o));
+  const int arc = (flags & SBX_FLAG_EXACT) ? c->pe->apply_exact(dp, o, c->stream)
+                                            : c->pe->apply(dp, o, c->stream);
+  if (arc != SBX_OK) {
+    set_error(c->pe->error());
+    return (sbx_status)arc;
+  }
+  if (!odev)
+    SBX_CUDA(cudaMemcpyAsync(out, o, sizeof(double) * (size_t)c->pe->pnodes(),
+                             cudaMemcpyDeviceToHost, c->stream));
+  return finish(c);
+}
+
+sbx_status sbx_pressure_diagonal(sbx_ctx* c, double* diag, uint32_t flags) {
+  if (!diag) {
+    set_error("sbx_pressure_diagonal: null output");
+    return SBX_E_INVALID;
+  }
+  SBX_TRY(pressure_enter(c));
+  const bool ex = flags & SBX_FLAG_EXACT;
+  const int rc = ex ? c->pe->ensure_diag_exact(c->stream) : c->pe->ensure_diag(c->stream);
+  if (rc != SBX_OK) {
+    set_error(c->pe->error());
+    return (sbx_status)rc;
+  }
+  SBX_CUDA(cudaMemcpyAsync(diag, ex ? c->pe->diag_exact() : c->pe->diag(),
+                           sizeof(double) * (size_t)c->pe->pnodes(), cudaMemcpyDefault,
+                           c->stream));
+  return finish(c);
+}
+
+sbx_status sbx_pressure_pcg(sbx_ctx* c, const double* b, double* x, const sbx_pcg_config* cfg,
+                            sbx_pcg_result* res) {
+  if (!b || !x || !cfg || !res) {
+    set_error("sbx_pressure_pcg: null argument");
+    return SBX_E_INVALID;
+  }
+  SBX_TRY(pressure_enter(c));
+  const int64_t Np = c->pe->pnodes();
+  const double* db = nullptr;
+  SBX_TRY(stage_p(c, b, Np, 0, &db));
+  const bool xdev = is_device_ptr(x);
+  double* dx = x;
+  if (!xdev) {
+    SBX_TRY(work(c, 1, &dx));
+    SBX_CUDA(cudaMemcpyAsync(dx, x, sizeof(double) * (size_t)Np, cudaMemcpyHostToDevice,
+                             c->stream));
+  }
+  const int rc = cfg->mode == SBX_MODE_EXACT ? c->pe->solve_exact(c->stream, db, dx, *cfg, res)
+                                             : c->pe->solve(c->stream, db, dx, *cfg, res);
+  sbx_status st = (sbx_status)rc;
+  if (st == SBX_E_BREAKDOWN)
+    set_error("pcg: breakdown (p'Ap <= 0 or non-finite) at iteration " +
+              std::to_string(res->error_iteration));
+  else if (st == SBX_E_NAN)
+    set_error("pcg: residual diverged (NaN/Inf) at iteration " +
+              std::to_string(res->error_iteration));
+  else if (st != SBX_OK)
+    set_error(c->pe->error());
+  if (!xdev && (st == SBX_OK || st == SBX_E_BREAKDOWN || st == SBX_E_NAN)) {
+    SBX_CUDA(cudaMemcpyAsync(x, dx, sizeof(double) * (size_t)Np, cudaMemcpyDeviceToHost,
+                             c->stream));
+    const sbx_status f = finish(c);
+    if (st == SBX_OK) st = f;
+  }
+  return st;
 }
 
 sbx_status sbx_ctx_enable_timing(sbx_ctx* c, int enable) {

@@ -45,6 +45,7 @@ struct OpDev {
   // (see trilinear_coeffs) and the GLL nodes / weights, so the fused CG
   // kernel can form the metric at each node instead of streaming G
   const double* tl = nullptr;
+  const double* corners = nullptr;  // [E][8][3] (box / verified-hint contexts)
   double Xh[33], Wh[33];
   // lattice gather-scatter: mask / multiplicities / gs / rhs check derived
   // from the box lattice on the device (setup_dev.cu); no boundary CSR
@@ -76,6 +77,7 @@ struct CgScalars {
   // single-graph solve: what the device prologue found (kPre* bits)
   int32_t pre;
   int32_t pad_;
+  double mu;  // pressure CG: mean of r/diag (the deflated preconditioner)
 };
 // CgScalars::pre
 constexpr int kPreNonzeroX = 1;  // x0 != 0: r = b - A x0 needs the general path
@@ -193,6 +195,69 @@ cudaError_t launch_validate_box(const OpDev& op, int64_t G, const int64_t* offse
 cudaError_t launch_validate_geom(const double* corners, int64_t E, int n, const double* x,
                                  const double* w, const double* G, const double* bm, int* flag,
                                  cudaStream_t s);
+
+// ---- consistent-Poisson pressure operator (pressure.cu) --------------------
+// Element data of the P_N / P_N-2 pair: n = N+1 GLL, m = N-1 GL points; the
+// 1-D operators [I^T | (I D)^T | I | I D | GL w | GL x] (device) and the
+// trilinear map coefficients of every element (the GL metric is formed on
+// the fly).
+struct PresDev {
+  int n = 0, m = 0;
+  int64_t E = 0, Np = 0;  // elements, pressure nodes E*m^3
+  const double* tl = nullptr;
+  const double* mats = nullptr;
+};
+cudaError_t launch_p_grad(const PresDev& P, const double* p, double* const g[3], cudaStream_t s);
+cudaError_t launch_p_div(const PresDev& P, const double* const v[3], double* q, cudaStream_t s);
+cudaError_t launch_p_diag(const PresDev& P, const double* inv_bdiag, double* diag,
+                          cudaStream_t s);
+// g_c := scale * gs_sum(g_c) for c = 0..2 (gather-scatter of the velocity-grid
+// gradient, then the masked inverse assembled mass; stepper.cpp:242-245)
+cudaError_t launch_gs3_scale(const OpDev& op, double* const g[3], const double* scale,
+                             cudaStream_t s);
+struct PIterArgs {
+  const OpDev* op;
+  const double* inv_bdiag;
+  double* r;
+  const double* dinv;  // null: no preconditioner (deflation only)
+  double* p;
+  double* x;
+  double* q;
+  double* g[3];
+  double* partials;
+  CgScalars* sc;
+  double* hist;
+  int64_t hist_cap;
+};
+// EXACT (reference-order) pressure operators (pressure_exact.cu)
+struct PresExact {
+  int n = 0, m = 0;
+  int64_t E = 0;
+  const double* corners = nullptr;  // [E][8][3]
+  const double* d = nullptr;        // GLL derivative n x n
+  const double* iv = nullptr;       // interp_v2p m x n
+  const double* ivt = nullptr;      // n x m
+  const double* glx = nullptr;      // GL nodes
+  const double* glw = nullptr;      // GL weights
+};
+cudaError_t launch_p_grad_exact(const PresExact& X, const double* p, double* const g[3],
+                                cudaStream_t s);
+cudaError_t launch_p_div_exact(const PresExact& X, const double* const u[3], double* out,
+                               cudaStream_t s);
+cudaError_t launch_p_diag_exact(const PresExact& X, const double* inv_bdiag, double* diag,
+                                cudaStream_t s);
+// z -= mean(z) with the mean summed sequentially (stepper.cpp:278-283)
+cudaError_t launch_deflate_exact(int64_t N, double* z, double* mean_scratch, cudaStream_t s);
+// field_dot (field.cpp:59-67): per-element sequential partials, serial sum
+cudaError_t launch_dot_exact_n(int64_t E, int nper, const double* a, const double* b,
+                               double* partials, double* out, cudaStream_t s);
+cudaError_t launch_p_iteration(const PresDev& P, const PIterArgs& A,
+                               cudaGraphConditionalHandle cond, int use_cond, cudaStream_t s);
+// out[8] = [b'b, b'(b/d), sum b/d, sum b, r'(r/d), sum r/d, sum r, r'r]
+cudaError_t launch_p_init(const PresDev& P, const double* b, const double* r, const double* dinv,
+                          double* partials, uint32_t* counter, double* out, cudaStream_t s);
+cudaError_t launch_p_finish(const PresDev& P, const double* p, double* x, const CgScalars* sc,
+                            cudaStream_t s);
 
 // ---- fused FAST CG (cg.cu) -------------------------------------------------
 // Whether the multi-GPU solver has a pipelined K1 (the halo leaves from its

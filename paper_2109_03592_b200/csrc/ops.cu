@@ -448,6 +448,13 @@ cudaError_t launch_gs(const OpDev& op, double* f, bool apply_mask, cudaStream_t 
   return cudaGetLastError();
 }
 
+cudaError_t launch_dot_exact_n(int64_t E, int nper, const double* a, const double* b,
+                               double* partials, double* out, cudaStream_t s) {
+  dot_elem_kernel<<<(unsigned)((E + 127) / 128), 128, 0, s>>>(a, b, nullptr, E, nper, partials);
+  serial_sum_kernel<<<1, 1, 0, s>>>(partials, E, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_dot_exact(const OpDev& op, const double* a, const double* b,
                              const double* w, double* partials, double* out, cudaStream_t s) {
   const int nper = op.n * op.n * op.n;

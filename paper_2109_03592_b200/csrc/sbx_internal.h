@@ -18,6 +18,7 @@ void set_error(const std::string& msg);
 // host setup (setup.cpp)
 void host_parallel_for(int64_t n, const std::function<void(int64_t, int64_t)>& fn);
 int gll_basis(int degree, double* nodes, double* weights, double* deriv);
+int pressure_basis(int degree, double* nodes, double* weights, double* interp);
 int box_corners(int ex, int ey, int ez, const double* origin, const double* lengths,
                 double* corners);
 void deform_corners(int64_t elem_count, double a, double* corners);

@@ -122,6 +122,66 @@ int gll_basis(int degree, double* nodes, double* weights, double* deriv) {
   return SBX_OK;
 }
 
+// GL pressure basis of the P_N / P_N-2 pair (basis.cpp:114-145): the m = N-1
+// roots of L_m by Newton from the Chebyshev-like guesses, symmetrised, their
+// weights, and the velocity-to-pressure interpolation l_j(gl_i) in the
+// barycentric form of lagrange_eval (basis.cpp:147-162).
+int pressure_basis(int degree, double* nodes, double* weights, double* interp) {
+  if (degree < 3 || degree > kMaxDegree) return SBX_E_CONFIG;
+  const int m = degree - 1, n = degree + 1;
+  std::vector<double> x(m, 0.0), w(m, 0.0);
+  for (int i = 0; i < m; ++i) {
+    double xi = -std::cos(M_PI * (i + 0.75) / (m + 0.5));
+    for (int it = 0; it < 100; ++it) {
+      double p, dp;
+      legendre_pair(m, xi, p, dp);
+      const double dx = p / dp;
+      xi -= dx;
+      if (std::abs(dx) <= 1e-15) break;
+    }
+    x[i] = xi;
+  }
+  for (int i = 0; i < m / 2; ++i) {
+    const double half = 0.5 * (x[m - 1 - i] - x[i]);
+    x[i] = -half;
+    x[m - 1 - i] = half;
+  }
+  if (m % 2) x[m / 2] = 0.0;
+  for (int i = 0; i < m; ++i) {
+    double p, dp;
+    legendre_pair(m, x[i], p, dp);
+    w[i] = 2.0 / ((1.0 - x[i] * x[i]) * dp * dp);
+  }
+  std::vector<double> v(n);
+  gll_basis(degree, v.data(), nullptr, nullptr);
+  std::vector<double> bary(n, 1.0);
+  for (int j = 0; j < n; ++j)
+    for (int k = 0; k < n; ++k)
+      if (k != j) bary[j] /= (v[j] - v[k]);
+  for (int i = 0; i < m; ++i) {
+    double* row = interp ? interp + (size_t)i * n : nullptr;
+    if (!row) continue;
+    int hit = -1;
+    for (int j = 0; j < n; ++j)
+      if (x[i] == v[j]) {
+        hit = j;
+        break;
+      }
+    if (hit >= 0) {
+      for (int j = 0; j < n; ++j) row[j] = j == hit ? 1.0 : 0.0;
+      continue;
+    }
+    double denom = 0.0;
+    for (int j = 0; j < n; ++j) denom += bary[j] / (x[i] - v[j]);
+    for (int j = 0; j < n; ++j) row[j] = (bary[j] / (x[i] - v[j])) / denom;
+  }
+  for (int i = 0; i < m; ++i) {
+    if (nodes) nodes[i] = x[i];
+    if (weights) weights[i] = w[i];
+  }
+  return SBX_OK;
+}
+
 // ------------------------------------------------------------------- mesh --
 int box_corners(int ex, int ey, int ez, const double* origin, const double* lengths,
                 double* corners) {

@@ -237,6 +237,57 @@ __global__ void gs_box_kernel(BoxLat b, int n, int cols, double* __restrict__ f,
   }
 }
 
+// gs_sum of three fields, then the pointwise scale (every node, the element
+// interiors included): apply_pressure_operator's gradient step
+// (stepper.cpp:242-245).  Reference copy order, as gs_box_kernel.
+__global__ void gs3_scale_box_kernel(BoxLat b, int n, int cols, double* __restrict__ f0,
+                                     double* __restrict__ f1, double* __restrict__ f2,
+                                     const double* __restrict__ scale) {
+  const int N = n - 1, n3 = n * n * n;
+  for (int col = blockIdx.x * blockDim.x + threadIdx.x; col < cols;
+       col += gridDim.x * blockDim.x) {
+    const Col32 c = col_of(b, n, col);
+    const bool face = c.i == 0 || c.i == N || c.j == 0 || c.j == N;
+    for (int k = 0; k < n; ++k) {
+      const int a = c.e * n3 + (k * n + c.j) * n + c.i;
+      if (!face && k != 0 && k != N) {
+        const double w = scale[a];
+        f0[a] *= w;
+        f1[a] *= w;
+        f2[a] *= w;
+        continue;
+      }
+      int idx[8];
+      bool masked;
+      const int m = copies32(b, n, c, k, idx, masked);
+      if (idx[0] != a) continue;  // the group's first copy does the work
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+      for (int q = 0; q < m; ++q) {
+        s0 = __dadd_rn(s0, f0[idx[q]]);
+        s1 = __dadd_rn(s1, f1[idx[q]]);
+        s2 = __dadd_rn(s2, f2[idx[q]]);
+      }
+      for (int q = 0; q < m; ++q) {
+        const double w = scale[idx[q]];
+        f0[idx[q]] = __dmul_rn(s0, w);
+        f1[idx[q]] = __dmul_rn(s1, w);
+        f2[idx[q]] = __dmul_rn(s2, w);
+      }
+    }
+  }
+}
+
+__global__ void mul3_kernel(int64_t N, double* __restrict__ f0, double* __restrict__ f1,
+                            double* __restrict__ f2, const double* __restrict__ scale) {
+  for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < N;
+       a += (int64_t)gridDim.x * blockDim.x) {
+    const double w = scale[a];
+    f0[a] = __dmul_rn(f0[a], w);
+    f1[a] = __dmul_rn(f1[a], w);
+    f2[a] = __dmul_rn(f2[a], w);
+  }
+}
+
 // Continuity: every copy equals its face neighbours' copies (the copies of a
 // node are connected by face steps, so pairwise face equality is equality of
 // all copies); masked copies are zero.
@@ -405,6 +456,22 @@ cudaError_t launch_validate_geom(const double* corners, int64_t E, int n, const 
     q.w[i] = w[i];
   }
   validate_geom_kernel<<<grid_for(E * n * n * n), 256, 0, s>>>(corners, E, n, q, G, bm, flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gs3_scale(const OpDev& op, double* const g[3], const double* scale,
+                             cudaStream_t s) {
+  if (op.lat) {
+    const int cols = (int)(op.E * op.n * op.n);
+    gs3_scale_box_kernel<<<grid_for(cols), 256, 0, s>>>(box_lat(op), op.n, cols, g[0], g[1],
+                                                        g[2], scale);
+    return cudaGetLastError();
+  }
+  for (int c = 0; c < 3; ++c) {
+    const cudaError_t e = launch_gs(op, g[c], false, s);
+    if (e != cudaSuccess) return e;
+  }
+  mul3_kernel<<<grid_for(op.nodes), 256, 0, s>>>(op.nodes, g[0], g[1], g[2], scale);
   return cudaGetLastError();
 }
 

@@ -97,3 +97,21 @@ def test_rcb_octants_and_balance():
     for ranks in (2, 3, 4, 8, 16, 64):
         cnt = np.bincount(sb.partition_rcb(mesh, ranks), minlength=ranks)
         assert cnt.min() >= 1 and cnt.max() <= 2 * cnt.min()
+
+
+def test_pressure_basis_bitwise():
+    """build_pressure_basis (basis.cpp:114-145): GL nodes, weights and the
+    velocity-to-pressure interpolation, bitwise against the reference build."""
+    import pytest
+
+    from oracle import oracle as O
+
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    for N in (3, 4, 5, 7, 8, 9, 12, 15):
+        pb = sb.build_pressure_basis(N)
+        P = O.Problem(2, 1, 1, N, backend="ref")
+        P.pressure_setup()
+        assert np.array_equal(pb.nodes, P.pressure_array(0)), N
+        assert np.array_equal(pb.weights, P.pressure_array(1)), N
+        assert np.array_equal(pb.interp_v2p, P.pressure_array(2)), N
