@@ -255,6 +255,25 @@ sbx_status sbx_pressure_diagonal(sbx_ctx* ctx, double* diag, uint32_t flags);
 sbx_status sbx_pressure_pcg(sbx_ctx* ctx, const double* b, double* x, const sbx_pcg_config* cfg,
                             sbx_pcg_result* result);
 
+/* ProjectionHistory (krylov.hpp:45-64, krylov.cpp:93-124) of the pressure
+ * solve (stepper.cpp:326, 345): A-orthonormal (x, E x) pairs kept on the
+ * device, plain field_dot; depth 0 disables.  flags: SBX_FLAG_EXACT for the
+ * reference's evaluation order (bitwise), else FAST. */
+sbx_status sbx_projection_reset(sbx_ctx* ctx, int depth);
+sbx_status sbx_projection_size(sbx_ctx* ctx, int32_t* size);
+/* guess = sum_i (x_i . b) x_i; deflated_rhs (may be NULL) = b - E guess */
+sbx_status sbx_projection_guess(sbx_ctx* ctx, const double* b, double* guess,
+                                double* deflated_rhs, uint32_t flags);
+/* append a converged solution (A-orthonormalised; the oldest entry evicted) */
+sbx_status sbx_projection_append(sbx_ctx* ctx, const double* x, uint32_t flags);
+
+/* advect (operators.hpp:84-87, operators.cpp:412-431) with grad_velocity
+ * (:300-325): out_d = bm (c . grad u_d), d = 0..2, in the reference's
+ * evaluation order (bitwise; dr/dx formed at each GLL node from the element
+ * corners as build_geometric_factors does).  Velocity-grid fields. */
+sbx_status sbx_advect(sbx_ctx* ctx, const double* const u[3], const double* const c[3],
+                      double* const out[3]);
+
 /* -------------------------------------------------------- multi-GPU ------ */
 /* One process per GPU; elements of a structured box are partitioned by
  * partition_rcb (mesh.cpp:168-226).  Shared nodes on rank boundaries are

@@ -151,6 +151,11 @@ def _ref():
         L.ref_pressure_apply.argtypes = [_P, _dp, _dp]
         L.ref_pressure_pcg.argtypes = [_P, C.c_int, _dp, _dp, C.c_double, C.c_int, _i64p, _dp,
                                        _dp, C.c_int64, _i64p]
+        L.ref_projection_reset.argtypes = [_P, C.c_int]
+        L.ref_projection_size.argtypes = [_P]
+        L.ref_projection_guess.argtypes = [_P, _dp, _dp, C.c_void_p]
+        L.ref_projection_append.argtypes = [_P, _dp]
+        L.ref_advect.argtypes = [_P] + [_dp] * 9
         L.ref_bench_prepare.argtypes = [_P, C.c_double, C.c_double, _dp]
         L.ref_bench_solve.argtypes = [_P, C.c_int, _i64p, _dp]
         L.ref_dense_helmholtz_element.argtypes = [_P, C.c_int, C.c_double, C.c_double, _dp]
@@ -185,6 +190,7 @@ class Problem:
     lengths: tuple = (1.0, 1.0, 1.0)
     corners: np.ndarray | None = None
     backend: str = "port"  # "port" | "ref"
+    with_gradients: bool = False  # ref backend: GeometricFactors with drdx (advect)
     # filled in
     E: int = field(init=False)
     n: int = field(init=False)
@@ -238,7 +244,8 @@ class Problem:
         h = C.c_void_p()
         rc = L.ref_problem_create(self.ex, self.ey, self.ez, np.asarray(self.origin, np.float64),
                                   np.asarray(self.lengths, np.float64), self._per, self.degree,
-                                  self.corners.ctypes.data_as(C.c_void_p), 0, C.byref(h))
+                                  self.corners.ctypes.data_as(C.c_void_p),
+                                  int(self.with_gradients), C.byref(h))
         if rc:
             raise OracleError(rc, L.ref_last_error().decode())
         self._h = h
@@ -419,6 +426,34 @@ class Problem:
                                      cap, hlen)
         return PcgOut(int(info[0]), bool(info[1]), float(res[0]), float(res[1]),
                       hist[: min(int(hlen[0]), cap)].copy(), x, int(rc), int(info[2]))
+
+    def projection_reset(self, depth):
+        _ref().ref_projection_reset(self._h, depth)
+
+    def projection_size(self):
+        return _ref().ref_projection_size(self._h)
+
+    def projection_guess(self, b, deflated=False):
+        g = np.empty(self.pnodes_count)
+        d = np.empty(self.pnodes_count) if deflated else None
+        rc = _ref().ref_projection_guess(self._h, np.ascontiguousarray(b, np.float64), g,
+                                         None if d is None else d.ctypes.data_as(C.c_void_p))
+        if rc:
+            raise OracleError(rc, _ref().ref_last_error().decode())
+        return (g, d) if deflated else g
+
+    def projection_append(self, x):
+        rc = _ref().ref_projection_append(self._h, np.ascontiguousarray(x, np.float64))
+        if rc:
+            raise OracleError(rc, _ref().ref_last_error().decode())
+
+    def advect(self, u, c):
+        out = [np.empty(self.nodes_count) for _ in range(3)]
+        rc = _ref().ref_advect(self._h, *[np.ascontiguousarray(v, np.float64) for v in u],
+                               *[np.ascontiguousarray(v, np.float64) for v in c], *out)
+        if rc:
+            raise OracleError(rc, _ref().ref_last_error().decode())
+        return out
 
     def pressure_rhs(self, seed=5):
         """A pressure right-hand side as solve_pressure_update forms it

@@ -27,6 +27,7 @@
 #include <string>
 
 #include <algorithm>
+#include <memory>
 
 #include "sembox/basis.hpp"
 #include "sembox/errors.hpp"
@@ -66,6 +67,7 @@ struct Problem {
   double bench_h1 = 0.0, bench_h2 = 0.0;
   // consistent-Poisson pressure path (ref_pressure_setup)
   bool has_p = false;
+  std::unique_ptr<ProjectionHistory> proj;
   PressureBasis pb;
   PressureGeometry pg;
   Field inv_bdiag, pdiag;
@@ -512,6 +514,48 @@ int ref_pressure_pcg(void* h, int precond, const double* b, double* x, double to
       throw;
     }
     unwrap(xf, x);
+  });
+}
+
+// ProjectionHistory of the pressure solve (krylov.cpp:93-124) with the
+// pressure operator and field_dot, as solve_pressure_update uses it
+// (stepper.cpp:326, 345).
+void ref_projection_reset(void* h, int depth) {
+  static_cast<Problem*>(h)->proj.reset(new ProjectionHistory(depth));
+}
+int ref_projection_size(void* h) { return static_cast<Problem*>(h)->proj->size(); }
+int ref_projection_guess(void* h, const double* b, double* guess, double* deflated) {
+  auto* p = static_cast<Problem*>(h);
+  return guarded([&] {
+    const int m = p->pb.m();
+    Field bf(GridTag::pressure, p->mesh.elem_count, m), dfl;
+    std::memcpy(bf.v.data(), b, bf.v.size() * sizeof(double));
+    const Field g = p->proj->project_guess(bf, field_dot, deflated ? &dfl : nullptr);
+    unwrap(g, guess);
+    if (deflated) unwrap(dfl, deflated);
+  });
+}
+int ref_projection_append(void* h, const double* x) {
+  auto* p = static_cast<Problem*>(h);
+  return guarded([&] {
+    Field xf(GridTag::pressure, p->mesh.elem_count, p->pb.m());
+    std::memcpy(xf.v.data(), x, xf.v.size() * sizeof(double));
+    p->proj->append(xf, [p](const Field& in, Field& out) { pressure_apply(*p, in, out); },
+                    field_dot);
+  });
+}
+
+// advect (operators.cpp:412-431); the problem must be built with gradients
+int ref_advect(void* h, const double* u0, const double* u1, const double* u2, const double* c0,
+               const double* c1, const double* c2, double* o0, double* o1, double* o2) {
+  auto* p = static_cast<Problem*>(h);
+  return guarded([&] {
+    const VectorField u{wrap(*p, u0), wrap(*p, u1), wrap(*p, u2)};
+    const VectorField c{wrap(*p, c0), wrap(*p, c1), wrap(*p, c2)};
+    const VectorField o = advect(u, c, p->gf, p->basis);
+    unwrap(o[0], o0);
+    unwrap(o[1], o1);
+    unwrap(o[2], o2);
   });
 }
 

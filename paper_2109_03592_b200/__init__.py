@@ -19,9 +19,11 @@ from .api import (  # noqa: F401
     PcgResult,
     PressureBasis,
     PressureOperator,
+    ProjectionHistory,
     SemboxError,
     SolverError,
     SpectralBasis,
+    advect,
     axhelm,
     axhelm_diagonal,
     debug_cg_k1,

@@ -101,6 +101,11 @@ _sig("sbx_divergence_to_pressure", _i, _vp, _vp, _vp, _vp, _vp, _u32)
 _sig("sbx_pressure_apply", _i, _vp, _vp, _vp, _u32)
 _sig("sbx_pressure_diagonal", _i, _vp, _vp, _u32)
 _sig("sbx_pressure_pcg", _i, _vp, _vp, _vp, C.POINTER(PcgConfig), C.POINTER(PcgResultC))
+_sig("sbx_projection_reset", _i, _vp, _i)
+_sig("sbx_projection_size", _i, _vp, C.POINTER(_i32))
+_sig("sbx_projection_guess", _i, _vp, _vp, _vp, _vp, _u32)
+_sig("sbx_projection_append", _i, _vp, _vp, _u32)
+_sig("sbx_advect", _i, _vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp))
 
 FLAG_EXACT = 0x1
 FLAG_FLIP_T = 0x2

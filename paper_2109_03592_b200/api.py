@@ -647,3 +647,55 @@ def pcg_pressure(op: PressureOperator, b, x, cfg: KrylovConfig = KrylovConfig(),
     if hist is not None:
         out.residual_history = hist[: min(r.history_length, hist.size)].tolist()
     return out
+
+
+class ProjectionHistory:
+    """krylov.hpp:45-64 / krylov.cpp:93-124 on the pressure grid of ctx (the
+    pressure solve's initial-guess projection, stepper.cpp:326 and 345): the
+    A-orthonormal (x, E x) pairs stay on the device; plain field_dot."""
+
+    def __init__(self, ctx: Context, depth: int, exact: bool = False):
+        self.ctx = ctx
+        self.exact = exact
+        self.nodes = _pnodes(ctx)
+        _check(lib.sbx_projection_reset(ctx.handle, int(depth)))
+        self._depth = depth
+
+    def depth(self):
+        return self._depth
+
+    def size(self):
+        n = C.c_int32()
+        _check(lib.sbx_projection_size(self.ctx.handle, C.byref(n)))
+        return n.value
+
+    def project_guess(self, b, deflated_rhs=False):
+        """guess = sum_i (x_i . b) x_i [, b - E guess]"""
+        b = _f64(b)
+        _pshape(self.ctx, b)
+        new = (lambda: np.empty(self.nodes)) if isinstance(b, np.ndarray) else \
+            (lambda: b.new_empty(self.nodes))
+        guess = new()
+        defl = new() if deflated_rhs else None
+        _check(lib.sbx_projection_guess(self.ctx.handle, _ptr(b), _ptr(guess), _ptr(defl),
+                                        L.FLAG_EXACT if self.exact else 0))
+        return (guess, defl) if deflated_rhs else guess
+
+    def append(self, x):
+        x = _f64(x)
+        _pshape(self.ctx, x)
+        _check(lib.sbx_projection_append(self.ctx.handle, _ptr(x),
+                                         L.FLAG_EXACT if self.exact else 0))
+
+
+def advect(u, c, ctx: Context):
+    """operators.hpp:84-87 / operators.cpp:412-431: out_d = bm (c . grad u_d),
+    reference evaluation order (bitwise)."""
+    u = [_f64(v) for v in u]
+    c = [_f64(v) for v in c]
+    ctx._shape_check(*u, *c)
+    out = [np.empty(ctx.nodes) if isinstance(u[0], np.ndarray) else u[0].new_empty(ctx.nodes)
+           for _ in range(3)]
+    arr = lambda vs: (C.c_void_p * 3)(*[_ptr(v) for v in vs])  # noqa: E731
+    _check(lib.sbx_advect(ctx.handle, arr(u), arr(c), arr(out)))
+    return out

@@ -59,7 +59,7 @@ struct sbx_ctx {
   int64_t device_bytes = 0;
   // host copies kept for re-layout queries
   // scratch
-  double* work[6] = {};  // nodes-sized
+  double* work[10] = {};  // nodes-sized
   double* partials = nullptr;
   int64_t partials_len = 0;
   double* dscal = nullptr;   // 16 device doubles
@@ -82,6 +82,7 @@ struct sbx_ctx {
   void* window = nullptr;
   std::vector<int64_t> recv_base_for_src;  // per source rank, -1 if not a neighbour
   std::vector<void*> peer_windows;
+  double* dgllx = nullptr;  // GLL nodes on the device (advect)
   // timing
   bool timing = false;
   // a multi-GPU exchange timed out: the per-phase sequence counters of the
@@ -1339,6 +1340,108 @@ sbx_status sbx_pressure_pcg(sbx_ctx* c, const double* b, double* x, const sbx_pc
     if (st == SBX_OK) st = f;
   }
   return st;
+}
+
+sbx_status sbx_projection_reset(sbx_ctx* c, int depth) {
+  SBX_TRY(pressure_enter(c));
+  c->pe->proj_reset(depth);
+  return finish(c);
+}
+
+sbx_status sbx_projection_size(sbx_ctx* c, int32_t* size) {
+  SBX_TRY(pressure_enter(c));
+  if (size) *size = c->pe->proj_size();
+  return finish(c);
+}
+
+sbx_status sbx_projection_guess(sbx_ctx* c, const double* b, double* guess, double* deflated,
+                                uint32_t flags) {
+  if (!b || !guess) {
+    set_error("sbx_projection_guess: null field");
+    return SBX_E_INVALID;
+  }
+  SBX_TRY(pressure_enter(c));
+  const int64_t Np = c->pe->pnodes();
+  const double* db = nullptr;
+  SBX_TRY(stage_p(c, b, Np, 0, &db));
+  double* dg = guess;
+  const bool gdev = is_device_ptr(guess);
+  if (!gdev) SBX_TRY(work(c, 1, &dg));
+  double* dd = deflated;
+  const bool ddev = !deflated || is_device_ptr(deflated);
+  if (!ddev) SBX_TRY(work(c, 2, &dd));
+  const int rc = c->pe->proj_guess(c->stream, db, dg, dd, flags & SBX_FLAG_EXACT);
+  if (rc != SBX_OK) {
+    set_error(c->pe->error());
+    return (sbx_status)rc;
+  }
+  if (!gdev)
+    SBX_CUDA(cudaMemcpyAsync(guess, dg, sizeof(double) * (size_t)Np, cudaMemcpyDeviceToHost,
+                             c->stream));
+  if (!ddev)
+    SBX_CUDA(cudaMemcpyAsync(deflated, dd, sizeof(double) * (size_t)Np, cudaMemcpyDeviceToHost,
+                             c->stream));
+  return finish(c);
+}
+
+sbx_status sbx_projection_append(sbx_ctx* c, const double* x, uint32_t flags) {
+  if (!x) {
+    set_error("sbx_projection_append: null field");
+    return SBX_E_INVALID;
+  }
+  SBX_TRY(pressure_enter(c));
+  const double* dx = nullptr;
+  SBX_TRY(stage_p(c, x, c->pe->pnodes(), 0, &dx));
+  const int rc = c->pe->proj_append(c->stream, dx, flags & SBX_FLAG_EXACT);
+  if (rc != SBX_OK) {
+    set_error(c->pe->error());
+    return (sbx_status)rc;
+  }
+  return finish(c);
+}
+
+sbx_status sbx_advect(sbx_ctx* c, const double* const u[3], const double* const cv[3],
+                      double* const out[3]) {
+  SBX_TRY(check_ctx(c));
+  if (!u || !cv || !out) {
+    set_error("sbx_advect: null argument");
+    return SBX_E_INVALID;
+  }
+  for (int q = 0; q < 3; ++q)
+    if (!u[q] || !cv[q] || !out[q]) {
+      set_error("sbx_advect: null field");
+      return SBX_E_INVALID;
+    }
+  if (!c->op.corners || !c->op.bm) {
+    set_error("advect: needs the element corners and the mass factors (a box context or a "
+              "verified structured-box hint)");
+    return SBX_E_CONFIG;
+  }
+  SBX_TRY(enter(c));
+  const double* du[3];
+  const double* dc[3];
+  double* dout[3];
+  for (int q = 0; q < 3; ++q) {
+    SBX_TRY(stage_in(c, u[q], q, &du[q]));
+    SBX_TRY(stage_in(c, cv[q], 3 + q, &dc[q]));
+    dout[q] = out[q];
+    if (!is_device_ptr(out[q])) SBX_TRY(work(c, 6 + q, &dout[q]));
+  }
+  // GLL nodes on the device (the derivative matrix is op.Dd)
+  if (!c->dgllx) {
+    void* p = nullptr;
+    SBX_TRY(dalloc(c, &p, sizeof(double) * 33));
+    c->dgllx = static_cast<double*>(p);
+    SBX_CUDA(cudaMemcpyAsync(c->dgllx, c->op.Xh, sizeof(double) * c->op.n,
+                             cudaMemcpyHostToDevice, c->stream));
+  }
+  SBX_CUDA(launch_advect(c->op.E, c->op.n, c->op.corners, c->op.Dd, c->dgllx, c->op.bm, du, dc,
+                         dout, c->stream));
+  for (int q = 0; q < 3; ++q)
+    if (dout[q] != out[q])
+      SBX_CUDA(cudaMemcpyAsync(out[q], dout[q], sizeof(double) * (size_t)c->op.nodes,
+                               cudaMemcpyDeviceToHost, c->stream));
+  return finish(c);
 }
 
 sbx_status sbx_ctx_enable_timing(sbx_ctx* c, int enable) {

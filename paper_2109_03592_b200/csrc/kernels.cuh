@@ -246,6 +246,11 @@ cudaError_t launch_p_div_exact(const PresExact& X, const double* const u[3], dou
                                cudaStream_t s);
 cudaError_t launch_p_diag_exact(const PresExact& X, const double* inv_bdiag, double* diag,
                                 cudaStream_t s);
+// advect (operators.cpp:412-431): out_c = bm (c . grad u_c), reference order
+// (bitwise); D, gllx device arrays of the GLL basis
+cudaError_t launch_advect(int64_t E, int n, const double* corners, const double* D,
+                          const double* gllx, const double* bm, const double* const u[3],
+                          const double* const c[3], double* const out[3], cudaStream_t s);
 // z -= mean(z) with the mean summed sequentially (stepper.cpp:278-283)
 cudaError_t launch_deflate_exact(int64_t N, double* z, double* mean_scratch, cudaStream_t s);
 // field_dot (field.cpp:59-67): per-element sequential partials, serial sum

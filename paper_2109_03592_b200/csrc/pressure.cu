@@ -760,6 +760,11 @@ unsigned sgrid(int64_t N) {
 PressureEngine::~PressureEngine() {
   if (exec_) cudaGraphExecDestroy(exec_);
   if (graph_) cudaGraphDestroy(graph_);
+  for (auto& e : basis_) {
+    cudaFree(e.first);
+    cudaFree(e.second);
+  }
+  for (double* v : pool_) cudaFree(v);
   for (double* v : {mats_, inv_bdiag_, pdiag_, pdinv_, g_[0], g_[1], g_[2], r_, p_, q_,
                     partials_, hist_, sums_, xmats_, pdiag_x_, zx_, scal_})
     cudaFree(v);
@@ -1038,6 +1043,90 @@ int PressureEngine::solve_exact(cudaStream_t s, const double* b, double* x,
   res->rel_residual_precond = bmb > 0.0 ? std::sqrt(std::max(rz, 0.0) / bmb) : 0.0;
   res->converged = res->rel_residual <= cfg.tolerance &&
                    res->rel_residual_precond <= cfg.tolerance;
+  PE_CUDA(cudaStreamSynchronize(s));
+  return SBX_OK;
+}
+
+// ---- ProjectionHistory (krylov.cpp:93-124), plain field_dot ----------------
+int PressureEngine::pdot(cudaStream_t s, const double* a, const double* b, bool exact,
+                         double* out) {
+  if (!scal_) PE_CUDA(cudaMalloc(&scal_, 4 * sizeof(double)));
+  if (exact)
+    PE_CUDA(launch_dot_exact_n(P_.E, P_.m * P_.m * P_.m, a, b, partials_, scal_, s));
+  else
+    PE_CUDA(launch_dot_fast(P_.Np, a, b, nullptr, partials_, counter_ + 1, scal_, s));
+  PE_CUDA(cudaMemcpyAsync(out, scal_, sizeof(double), cudaMemcpyDeviceToHost, s));
+  PE_CUDA(cudaStreamSynchronize(s));
+  return SBX_OK;
+}
+
+int PressureEngine::proj_reset(int depth) {
+  for (auto& e : basis_) {
+    pool_.push_back(e.first);
+    pool_.push_back(e.second);
+  }
+  basis_.clear();
+  depth_ = depth;
+  return SBX_OK;
+}
+
+int PressureEngine::proj_guess(cudaStream_t s, const double* b, double* guess, double* deflated,
+                               bool exact) {
+  const int64_t Np = P_.Np;
+  PE_CUDA(cudaMemsetAsync(guess, 0, sizeof(double) * Np, s));
+  if (deflated && deflated != b)
+    PE_CUDA(cudaMemcpyAsync(deflated, b, sizeof(double) * Np, cudaMemcpyDeviceToDevice, s));
+  for (const auto& xy : basis_) {
+    double alpha;
+    if (pdot(s, xy.first, b, exact, &alpha)) return SBX_E_CUDA;
+    PE_CUDA(launch_axpy(Np, alpha, xy.first, guess, s));
+    if (deflated) PE_CUDA(launch_axpy(Np, -alpha, xy.second, deflated, s));
+  }
+  PE_CUDA(cudaStreamSynchronize(s));
+  return SBX_OK;
+}
+
+int PressureEngine::proj_append(cudaStream_t s, const double* x, bool exact) {
+  if (depth_ <= 0) return SBX_OK;
+  const int64_t Np = P_.Np;
+  auto fresh = [&](double** v) -> int {
+    if (!pool_.empty()) {
+      *v = pool_.back();
+      pool_.pop_back();
+      return SBX_OK;
+    }
+    PE_CUDA(cudaMalloc(v, sizeof(double) * Np));
+    return SBX_OK;
+  };
+  double *v = nullptr, *w = nullptr;
+  if (fresh(&v) || fresh(&w)) return SBX_E_CUDA;
+  PE_CUDA(cudaMemcpyAsync(v, x, sizeof(double) * Np, cudaMemcpyDeviceToDevice, s));
+  const int rc = exact ? apply_exact(x, w, s) : apply(x, w, s);
+  if (rc != SBX_OK) return rc;
+  double scale;
+  if (pdot(s, v, w, exact, &scale)) return SBX_E_CUDA;
+  for (const auto& xy : basis_) {
+    double c;
+    if (pdot(s, xy.first, w, exact, &c)) return SBX_E_CUDA;
+    PE_CUDA(launch_axpy(Np, -c, xy.first, v, s));
+    PE_CUDA(launch_axpy(Np, -c, xy.second, w, s));
+  }
+  double d;
+  if (pdot(s, v, w, exact, &d)) return SBX_E_CUDA;
+  if (!(d > scale * 1e-24) || !std::isfinite(d)) {  // linearly dependent
+    pool_.push_back(v);
+    pool_.push_back(w);
+    return SBX_OK;
+  }
+  const double inv = 1.0 / std::sqrt(d);
+  PE_CUDA(launch_scale(Np, inv, v, s));
+  PE_CUDA(launch_scale(Np, inv, w, s));
+  basis_.push_back({v, w});
+  while ((int)basis_.size() > depth_) {
+    pool_.push_back(basis_.front().first);
+    pool_.push_back(basis_.front().second);
+    basis_.pop_front();
+  }
   PE_CUDA(cudaStreamSynchronize(s));
   return SBX_OK;
 }

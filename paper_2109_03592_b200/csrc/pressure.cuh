@@ -6,7 +6,10 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <deque>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "../../include/sbx.h"
 #include "kernels.cuh"
@@ -33,6 +36,12 @@ class PressureEngine {
   const double* diag_exact() const { return pdiag_x_; }
   int solve_exact(cudaStream_t s, const double* b, double* x, const sbx_pcg_config& cfg,
                   sbx_pcg_result* res);
+  // ProjectionHistory (krylov.cpp:93-124) on the pressure grid: the
+  // A-orthonormal (x, E x) pairs live on the device
+  int proj_reset(int depth);
+  int proj_guess(cudaStream_t s, const double* b, double* guess, double* deflated, bool exact);
+  int proj_append(cudaStream_t s, const double* x, bool exact);
+  int proj_size() const { return (int)basis_.size(); }
   const double* diag() const { return pdiag_; }
   int64_t pnodes() const { return P_.Np; }
   int m1d() const { return P_.m; }
@@ -66,6 +75,11 @@ class PressureEngine {
   cudaGraph_t graph_ = nullptr;
   cudaGraphExec_t exec_ = nullptr;
   const void* gkey_[4] = {};
+  int pdot(cudaStream_t s, const double* a, const double* b, bool exact, double* out);
+  std::deque<std::pair<double*, double*>> basis_;
+  std::vector<double*> pool_;
+  int depth_ = 0;
+  double *pv_ = nullptr, *pw_ = nullptr;  // append scratch
   std::string err_;
 };
 
