@@ -274,6 +274,18 @@ sbx_status sbx_projection_append(sbx_ctx* ctx, const double* x, uint32_t flags);
 sbx_status sbx_advect(sbx_ctx* ctx, const double* const u[3], const double* const c[3],
                       double* const out[3]);
 
+/* Batched velocity solve (FlowSolver::solve_velocity_star, stepper.cpp:188-238):
+ * count <= 3 right-hand sides b[d] with the SAME operator / preconditioner
+ * (cfg: h1, h2, tolerance, max_iterations, precond), each with its own initial
+ * guess in x[d] (the previous velocity) and its own convergence; results[d]
+ * per component.  FAST: one graph -- every component's initial residual
+ * b - A x0 computed in the graph, then K1 / K2 launched once per iteration for
+ * all components (grid.y = component); per component the arithmetic of
+ * sbx_pcg.  EXACT: the components one after the other.  history, when given,
+ * holds count * history_capacity entries (component-major). */
+sbx_status sbx_pcg_multi(sbx_ctx* ctx, int count, const double* const* b, double* const* x,
+                         const sbx_pcg_config* cfg, sbx_pcg_result* results);
+
 /* -------------------------------------------------------- multi-GPU ------ */
 /* One process per GPU; elements of a structured box are partitioned by
  * partition_rcb (mesh.cpp:168-226).  Shared nodes on rank boundaries are

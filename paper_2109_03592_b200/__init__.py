@@ -41,6 +41,7 @@ from .api import (  # noqa: F401
     gs_sum_inplace,
     partition_rcb,
     pcg,
+    pcg_multi,
     pcg_pressure,
 )
 

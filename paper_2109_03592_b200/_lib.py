@@ -106,6 +106,8 @@ _sig("sbx_projection_size", _i, _vp, C.POINTER(_i32))
 _sig("sbx_projection_guess", _i, _vp, _vp, _vp, _vp, _u32)
 _sig("sbx_projection_append", _i, _vp, _vp, _u32)
 _sig("sbx_advect", _i, _vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp))
+_sig("sbx_pcg_multi", _i, _vp, _i, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(PcgConfig),
+     C.POINTER(PcgResultC))
 
 FLAG_EXACT = 0x1
 FLAG_FLIP_T = 0x2

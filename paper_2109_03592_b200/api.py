@@ -699,3 +699,45 @@ def advect(u, c, ctx: Context):
     arr = lambda vs: (C.c_void_p * 3)(*[_ptr(v) for v in vs])  # noqa: E731
     _check(lib.sbx_advect(ctx.handle, arr(u), arr(c), arr(out)))
     return out
+
+
+def pcg_multi(op: HelmholtzOperator, bs, xs, cfg: KrylovConfig = KrylovConfig(),
+              precond: Optional[str] = "jacobi", mode: str = "fast", history=True):
+    """FlowSolver::solve_velocity_star's three component solves
+    (stepper.cpp:188-238) as one batched call: bs[d], xs[d] (initial guess in,
+    solution out), the same operator and KrylovConfig for every component.
+    Returns one PcgResult per component."""
+    if not op.use_mask:
+        raise ContractViolation("pcg: HelmholtzOperator(use_mask=False) is not supported")
+    count = len(bs)
+    if count != len(xs) or not 1 <= count <= 3:
+        raise ContractViolation("pcg_multi: 1 to 3 right-hand sides, one x each")
+    bs = [_f64(b) for b in bs]
+    op.ctx._shape_check(*bs, *xs)
+    c = L.PcgConfig()
+    lib.sbx_pcg_config_default(C.byref(c))
+    c.tolerance = cfg.tolerance
+    c.max_iterations = cfg.max_iterations
+    c.precond = L.PRECOND_JACOBI if precond == "jacobi" else L.PRECOND_NONE
+    c.mode = L.MODE_EXACT if mode == "exact" else L.MODE_FAST
+    c.h1 = op.coeffs.h1
+    c.h2 = op.coeffs.h2
+    hist = None
+    cap = max(cfg.max_iterations, 0) + 1
+    if history:
+        hist = np.zeros(count * cap)
+        c.history = hist.ctypes.data
+        c.history_capacity = cap
+    res = (L.PcgResultC * count)()
+    barr = (C.c_void_p * count)(*[_ptr(b) for b in bs])
+    xarr = (C.c_void_p * count)(*[_ptr(x) for x in xs])
+    rc = lib.sbx_pcg_multi(op.ctx.handle, count, barr, xarr, C.byref(c), res)
+    err_it = max((r.error_iteration for r in res), default=-1)
+    _check(rc, err_it)
+    out = []
+    for d, r in enumerate(res):
+        o = PcgResult(r.iterations, r.rel_residual, r.rel_residual_precond, bool(r.converged))
+        if hist is not None:
+            o.residual_history = hist[d * cap: d * cap + min(r.history_length, cap)].tolist()
+        out.append(o)
+    return out

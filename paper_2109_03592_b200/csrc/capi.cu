@@ -484,6 +484,11 @@ sbx_status ensure_diag(sbx_ctx* c, double h1, double h2) {
   return SBX_OK;
 }
 
+sbx_status ensure_diag_if(sbx_ctx* c, const sbx_pcg_config* cfg) {
+  if (cfg->precond == SBX_PRECOND_JACOBI) return ensure_diag(c, cfg->h1, cfg->h2);
+  return SBX_OK;
+}
+
 // ---- EXACT PCG: krylov.cpp:7-91 statement by statement ------------------
 sbx_status pcg_exact(sbx_ctx* c, const double* b, double* x, const sbx_pcg_config* cfg,
                      sbx_pcg_result* res) {
@@ -1442,6 +1447,87 @@ sbx_status sbx_advect(sbx_ctx* c, const double* const u[3], const double* const 
       SBX_CUDA(cudaMemcpyAsync(out[q], dout[q], sizeof(double) * (size_t)c->op.nodes,
                                cudaMemcpyDeviceToHost, c->stream));
   return finish(c);
+}
+
+// Batched solve of count <= 3 right-hand sides with one operator: the three
+// velocity components of FlowSolver::solve_velocity_star (stepper.cpp:
+// 188-238), each with its own initial guess in x[d] and its own convergence.
+sbx_status sbx_pcg_multi(sbx_ctx* c, int count, const double* const* b, double* const* x,
+                         const sbx_pcg_config* cfg, sbx_pcg_result* res) {
+  SBX_TRY(check_ctx(c));
+  if (!b || !x || !cfg || !res || count < 1 || count > kMaxComp) {
+    set_error("sbx_pcg_multi: null argument or count not in [1, 3]");
+    return SBX_E_INVALID;
+  }
+  for (int q = 0; q < count; ++q)
+    if (!b[q] || !x[q]) {
+      set_error("sbx_pcg_multi: null field");
+      return SBX_E_INVALID;
+    }
+  if (cfg->h2 != 0.0 && !c->op.bm) {
+    set_error("pcg: h2 != 0 needs the mass factors (bm)");
+    return SBX_E_SHAPE;
+  }
+  auto one = [&](int q) -> sbx_status {
+    sbx_pcg_config cq = *cfg;
+    if (cfg->history) cq.history = cfg->history + (size_t)q * cfg->history_capacity;
+    return sbx_pcg(c, b[q], x[q], &cq, &res[q]);
+  };
+  if (cfg->mode != SBX_MODE_FAST || c->dist || count == 1) {
+    // reference order (or one rhs): the components one after the other, as
+    // solve_velocity_star does
+    for (int q = 0; q < count; ++q) SBX_TRY(one(q));
+    return SBX_OK;
+  }
+  SBX_TRY(enter(c));
+  const int64_t N = c->op.nodes;
+  SBX_TRY(ensure_diag_if(c, cfg));
+  const double* db[kMaxComp];
+  double* dx[kMaxComp];
+  bool xdev[kMaxComp];
+  for (int q = 0; q < count; ++q) {
+    SBX_TRY(stage_in(c, b[q], q, &db[q]));
+    xdev[q] = is_device_ptr(x[q]);
+    dx[q] = x[q];
+    if (!xdev[q]) {
+      SBX_TRY(work(c, 3 + q, &dx[q]));
+      SBX_CUDA(cudaMemcpyAsync(dx[q], x[q], sizeof(double) * (size_t)N, cudaMemcpyHostToDevice,
+                               c->stream));
+    }
+  }
+  CgRun runs[kMaxComp];
+  for (int q = 0; q < count; ++q) {
+    CgRun& r = runs[q];
+    r.op = &c->op;
+    r.stream = c->stream;
+    r.b = db[q];
+    r.x = dx[q];
+    r.dinv = cfg->precond == SBX_PRECOND_JACOBI ? c->ddinv : nullptr;
+    r.h1 = cfg->h1;
+    r.h2 = cfg->h2;
+    r.tol = cfg->tolerance;
+    r.max_it = cfg->max_iterations;
+    r.history = cfg->history ? cfg->history + (size_t)q * cfg->history_capacity : nullptr;
+    r.history_capacity = cfg->history_capacity;
+    r.interior_clean = c->interior_clean;
+  }
+  const int rc = c->cg->solve_multi(runs, count, res);
+  if (rc == kCgFallback) {
+    // no batched kernels here (or a right-hand side the fused schedule cannot
+    // take): nothing was written; solve the components one by one
+    for (int q = 0; q < count; ++q) SBX_TRY(one(q));
+    return SBX_OK;
+  }
+  sbx_status st = (sbx_status)rc;
+  if (st == SBX_E_CUDA) set_error(c->cg->error());
+  else if (st == SBX_E_BREAKDOWN || st == SBX_E_NAN)
+    set_error("pcg (batched): breakdown or NaN/Inf in a component");
+  for (int q = 0; q < count; ++q)
+    if (!xdev[q])
+      SBX_CUDA(cudaMemcpyAsync(x[q], dx[q], sizeof(double) * (size_t)N, cudaMemcpyDeviceToHost,
+                               c->stream));
+  const sbx_status f = finish(c);
+  return st == SBX_OK ? f : st;
 }
 
 sbx_status sbx_ctx_enable_timing(sbx_ctx* c, int enable) {

@@ -103,8 +103,19 @@ struct CgK1Pol {
     int par;  // send-buffer parity of this iteration's halo (phase 0)
     const int32_t* esend_off;
     int stored;  // this thread pushed halo values (fence before the ticket)
+    const CgMulti* multi;  // batched solve: this CTA's component is blockIdx.y
+    int64_t part_off;
   };
   __device__ static bool init(Args& a) {
+    if (a.multi) {
+      const int c = blockIdx.y;
+      a.r = a.multi->r[c];
+      a.p = a.multi->p[c];
+      a.x = a.multi->x[c];
+      a.w = a.multi->w[c];
+      a.sc = a.multi->sc[c];
+      a.part_off = c * a.multi->part_stride;
+    }
     if (a.sc->done) return false;
     a.first = a.sc->first;
     a.beta = a.sc->beta;
@@ -183,6 +194,7 @@ __device__ void CgK1Pol<HAS_DINV, HAS_BM>::finish(const Args& a, double red, dou
   // system scope once, here, before the CTA's ticket; the last CTA then
   // releases them with dist_release_phase0)
   if (a.stored) __threadfence_system();
+  partials += a.part_off;
   const double v = cta_sum(red, sh);
   if (threadIdx.x == 0) partials[blockIdx.x] = v;
   CgScalars* sc = a.sc;
@@ -302,7 +314,8 @@ __device__ __forceinline__ void update_tail(double rz, double rr, double alpha, 
                                             double* __restrict__ partials,
                                             double* __restrict__ hist, int64_t hist_cap,
                                             cudaGraphConditionalHandle cond, int use_cond,
-                                            const DistDev* dd = nullptr) {
+                                            const DistDev* dd = nullptr,
+                                            const CgMulti* multi = nullptr) {
   rz = cta_sum(rz, red);
   const double rz_b = rz;
   rr = cta_sum(rr, red);
@@ -348,7 +361,7 @@ __device__ __forceinline__ void update_tail(double rz, double rr, double alpha, 
         sc->done = 1;
       }
     }
-    if (use_cond) cudaGraphSetConditional(cond, sc->done ? 0 : 1);
+    if (use_cond) cudaGraphSetConditional(cond, (multi ? multi_active(multi) : !sc->done) ? 1 : 0);
   }
 }
 
@@ -636,7 +649,8 @@ __global__ void __launch_bounds__(K2Layout<n, GROUPS, SPG>::threads, 1)
                          const int32_t* __restrict__ nbr27, const DistDev* __restrict__ dd,
                          CgScalars* __restrict__ sc, double* __restrict__ partials,
                          double* __restrict__ hist, int64_t hist_cap,
-                         cudaGraphConditionalHandle cond, int use_cond) {
+                         cudaGraphConditionalHandle cond, int use_cond,
+                         const CgMulti* __restrict__ multi) {
   using T = K2Geom<n>;
   using L = K2Layout<n, GROUPS, SPG>;
   using St = K2Stage<n>;
@@ -646,8 +660,18 @@ __global__ void __launch_bounds__(K2Layout<n, GROUPS, SPG>::threads, 1)
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ double red[32];
   __shared__ bool is_last;
+  if (multi) {
+    const int c = blockIdx.y;
+    w = multi->w[c];
+    r = multi->r[c];
+    sc = multi->sc[c];
+    hist = multi->hist[c];
+    partials += c * multi->part_stride;
+  }
   if (sc->done) {
-    if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0);
+    if (use_cond && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 &&
+        !(multi && multi_active(multi)))
+      cudaGraphSetConditional(cond, 0);
     return;
   }
   const double alpha = sc->alpha;
@@ -860,7 +884,8 @@ __global__ void __launch_bounds__(K2Layout<n, GROUPS, SPG>::threads, 1)
       if (lt == 0) mbar_arrive(&empty[s]);
     }
   }
-  update_tail(rz, rr, alpha, red, &is_last, sc, partials, hist, hist_cap, cond, use_cond, dd);
+  update_tail(rz, rr, alpha, red, &is_last, sc, partials, hist, hist_cap, cond, use_cond, dd,
+              multi);
 }
 
 template <int n>
@@ -969,8 +994,11 @@ __global__ void cg_init_kernel(int64_t N, const double* __restrict__ b,
 // (krylov.cpp:19-32); the last CTA sets up the device scalars exactly as the
 // host would (krylov.cpp:11-50) -- or flags why the general path is needed --
 // so the whole solve runs from one graph launch with one host sync.
+// q (optional) = A x0, computed in the same graph: r = b - q (the batched
+// solves always apply A to their initial guess; for x0 = 0 this is r = b
+// bit for bit).  x (optional) is scanned for nonzeros when q is absent.
 __global__ void cg_prologue_kernel(int64_t N, const double* __restrict__ b,
-                                   const double* __restrict__ x,
+                                   const double* __restrict__ x, const double* __restrict__ q,
                                    const double* __restrict__ dinv,
                                    const double* __restrict__ wgt, double* __restrict__ r,
                                    double* __restrict__ partials, CgScalars* __restrict__ sc,
@@ -978,25 +1006,31 @@ __global__ void cg_prologue_kernel(int64_t N, const double* __restrict__ b,
                                    const int* __restrict__ rhs_flag) {
   __shared__ double red[32];
   __shared__ bool is_last;
-  double s0 = 0.0, s1 = 0.0;
+  double s[4] = {0.0, 0.0, 0.0, 0.0};
   bool nz = false;
   for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < N;
        a += (int64_t)gridDim.x * blockDim.x) {
     const double bv = b[a], wv = wgt[a];
-    r[a] = bv;
+    const double rv = q ? bv - q[a] : bv;
+    r[a] = rv;
     const double di = dinv ? dinv[a] : 1.0;
-    s0 += bv * bv * wv;
-    s1 += bv * (bv * di) * wv;
-    nz |= (x[a] != 0.0);  // NaN counts as nonzero, as in the reference
+    s[0] += bv * bv * wv;
+    s[1] += bv * (bv * di) * wv;
+    s[2] += rv * (rv * di) * wv;
+    s[3] += rv * rv * wv;
+    if (x) nz |= (x[a] != 0.0);  // NaN counts as nonzero, as in the reference
   }
   if (__syncthreads_or(nz) && threadIdx.x == 0) atomicOr(&sc->pre, kPreNonzeroX);
-  const double v0 = cta_sum(s0, red);
-  if (threadIdx.x == 0) partials[2 * (int64_t)blockIdx.x] = v0;
-  const double v1 = cta_sum(s1, red);
-  if (threadIdx.x == 0) partials[2 * (int64_t)blockIdx.x + 1] = v1;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const double v = cta_sum(s[c], red);
+    if (threadIdx.x == 0) partials[4 * (int64_t)blockIdx.x + c] = v;
+  }
   if (!last_block(&sc->counter[2], &is_last)) return;
-  const double bb = reduce_partials(partials, gridDim.x, 2, 0, red);
-  const double bmb = reduce_partials(partials, gridDim.x, 2, 1, red);
+  const double bb = reduce_partials(partials, gridDim.x, 4, 0, red);
+  const double bmb = reduce_partials(partials, gridDim.x, 4, 1, red);
+  const double rz0 = reduce_partials(partials, gridDim.x, 4, 2, red);
+  const double rr0 = reduce_partials(partials, gridDim.x, 4, 3, red);
   if (threadIdx.x != 0) return;
   sc->counter[2] = 0;
   int pre = *(volatile int*)&sc->pre;
@@ -1016,12 +1050,11 @@ __global__ void cg_prologue_kernel(int64_t N, const double* __restrict__ b,
     sc->done = 1;
     return;
   }
-  // r = b (zero guess): rr = b'Wb, rz = b'W(M b)
-  const double bnorm = sqrt(bb), rnorm = sqrt(bb);
+  const double bnorm = sqrt(bb), rnorm = sqrt(rr0);
   const double rel0 = rnorm / bnorm;
-  const double relp0 = bmb > 0.0 ? sqrt(fmax(bmb, 0.0) / bmb) : 0.0;
-  sc->rz = bmb;
-  sc->rr = bb;
+  const double relp0 = bmb > 0.0 ? sqrt(fmax(rz0, 0.0) / bmb) : 0.0;
+  sc->rz = rz0;
+  sc->rr = rr0;
   sc->bnorm = bnorm;
   sc->bmb = bmb;
   sc->rel = rel0;
@@ -1095,6 +1128,12 @@ int num_sms(int dev) {
 #endif
 constexpr int tri_max_groups(int n) { return n <= 8 ? SBX_TRI_G8 : (n <= 12 ? SBX_TRI_G12 : 1); }
 
+// Batched (multi-right-hand-side) launches: while a batched solve captures its
+// graph, the K1 / K2 launchers below run their kernels with grid.y = ncomp
+// and the device CgMulti (set by CgEngine::solve_multi on this thread).
+thread_local const CgMulti* t_multi = nullptr;
+thread_local int t_ncomp = 1;
+
 // TRI: the metric is formed at each node from the element's trilinear map
 // (op.tl) instead of streaming the 6 stored factors -- 48 fewer bytes per
 // node on an HBM-bound kernel, for ~50 more FP64 operations per node.
@@ -1124,11 +1163,12 @@ cudaError_t launch_k1_tma(const OpDev& op, const double* r, const double* dinv, 
       Qp.w[q] = op.Wh[q];
     }
     typename Pol::Args a{r, dinv, p, x, w, op.bm, h2, sc, op.dd, 0.0, 0.0, 0, 0, nullptr, 0};
+    a.multi = t_multi;
     const int64_t NG = (op.E + TmaGeom<n>::EPG - 1) / TmaGeom<n>::EPG;
     int64_t grid = num_sms(dev);
     if (grid > NG) grid = NG;
-    kern<<<(unsigned)grid, L::threads, L::smem, s>>>(a, TRI ? op.tl : op.G, op.E, h1, 1.0, Dp,
-                                                     partials, Qp);
+    kern<<<dim3((unsigned)grid, t_ncomp), L::threads, L::smem, s>>>(
+        a, TRI ? op.tl : op.G, op.E, h1, 1.0, Dp, partials, Qp);
     return cudaGetLastError();
   }
 }
@@ -1160,9 +1200,11 @@ cudaError_t launch_k1_dmma(const OpDev& op, const double* r, const double* dinv,
       Qp.w[q] = op.Wh[q];
     }
     typename Pol::Args a{r, dinv, p, x, w, op.bm, h2, sc, op.dd, 0.0, 0.0, 0, 0, nullptr, 0};
+    a.multi = t_multi;
     int64_t grid = num_sms(dev);
     if (grid > op.E) grid = op.E;
-    kern<<<(unsigned)grid, L::threads, L::smem, s>>>(a, op.tl, op.E, h1, Dp, partials, Qp);
+    kern<<<dim3((unsigned)grid, t_ncomp), L::threads, L::smem, s>>>(a, op.tl, op.E, h1, Dp,
+                                                                     partials, Qp);
     return cudaGetLastError();
   }
 }
@@ -1214,8 +1256,9 @@ cudaError_t launch_k1(const OpDev& op, const double* r, const double* dinv, doub
     }
     if (tri && e == cudaErrorNotSupported) e = go(std::true_type{});
     if (e == cudaErrorNotSupported) e = go(std::false_type{});
-    if (e != cudaErrorNotSupported || op.dd) return e;
+    if (e != cudaErrorNotSupported || op.dd || t_multi) return e;
   }
+  if (t_multi) return cudaErrorNotSupported;  // batched: pipelined kernels only
   static std::atomic<bool> attr_set[64];  // per device (distinct contexts may race: idempotent)
   if (!attr_set[dev & 63]) {
     cudaError_t err = cudaFuncSetAttribute(
@@ -1256,13 +1299,15 @@ cudaError_t launch_k2(const OpDev& op, const double* w, double* r, const double*
     int64_t grid = num_sms(dev);
     if (grid > NG) grid = NG;
     BoxP bx{op.ex, op.ey, op.ez, op.per[0], op.per[1], op.per[2]};
-    kern<<<(unsigned)grid, L::threads, L::smem, s>>>(w, r, dinv, op.E, bx, op.nbr27, op.dd, sc,
-                                                     partials, hist, hist_cap, cond, use_cond);
+    kern<<<dim3((unsigned)grid, t_ncomp), L::threads, L::smem, s>>>(
+        w, r, dinv, op.E, bx, op.nbr27, op.dd, sc, partials, hist, hist_cap, cond, use_cond,
+        t_multi);
     return cudaGetLastError();
   }
   // multi-GPU: only the table-driven TMA kernel knows remote neighbours (-2),
-  // local element renumbering and the cross-rank r'z / r'r exchange
-  if (op.dd) return cudaErrorNotSupported;
+  // local element renumbering and the cross-rank r'z / r'r exchange (and
+  // only it runs batched solves)
+  if (op.dd || t_multi) return cudaErrorNotSupported;
   if (op.box) {
     using C = AxCfg<n>;
     static std::atomic<int> per_sm[64];
@@ -1431,6 +1476,21 @@ int cg_unroll() {
 }
 
 CgEngine::~CgEngine() {
+  if (mexec_) cudaGraphExecDestroy(mexec_);
+  if (mgraph_) cudaGraphDestroy(mgraph_);
+  for (int c = 0; c < kMaxComp; ++c) {
+    cudaFree(mr_[c]);
+    cudaFree(mp_[c]);
+    cudaFree(mw_[c]);
+    cudaFree(mhist_[c]);
+  }
+  cudaFree(msc_);
+  cudaFree(mpart_);
+  cudaFree(mflag_);
+  cudaFree(mprm_);
+  cudaFree(dmulti_);
+  if (mhsc_) cudaFreeHost(mhsc_);
+  if (mhprm_) cudaFreeHost(mhprm_);
   if (exec_) cudaGraphExecDestroy(exec_);
   if (graph_) cudaGraphDestroy(graph_);
   cudaFree(r_);
@@ -1567,8 +1627,9 @@ int CgEngine::build_solve_graph(const CgRun& run) {
   {
     int64_t blocks = std::min<int64_t>((N + 1023) / 1024, 1184);
     if (blocks < 1) blocks = 1;
-    cg_prologue_kernel<<<(unsigned)blocks, 256, 0, s>>>(N, run.b, run.x, run.dinv, op.inv_mult,
-                                                        r_, partials_, sc_, prm_, hist_, flag_);
+    cg_prologue_kernel<<<(unsigned)blocks, 256, 0, s>>>(N, run.b, run.x, nullptr, run.dinv,
+                                                        op.inv_mult, r_, partials_, sc_, prm_,
+                                                        hist_, flag_);
   }
   const cudaError_t ep = cudaGetLastError();
   CG_CUDA(cudaStreamEndCapture(s, &pre));
@@ -1643,6 +1704,211 @@ int CgEngine::solve_graph(const CgRun& run, sbx_pcg_result* res, bool* general) 
     return SBX_OK;
   }
   return collect(run, res);
+}
+
+int CgEngine::ensure_multi(const CgRun& run, int count) {
+  const OpDev& op = *run.op;
+  if (mop_ != run.op) {
+    for (int c = 0; c < kMaxComp; ++c) {
+      cudaFree(mr_[c]);
+      cudaFree(mp_[c]);
+      cudaFree(mw_[c]);
+      mr_[c] = mp_[c] = mw_[c] = nullptr;
+    }
+    mcount_ = 0;
+    mop_ = run.op;
+    if (mexec_) cudaGraphExecDestroy(mexec_);
+    mexec_ = nullptr;
+  }
+  for (int c = mcount_; c < count; ++c) {
+    CG_CUDA(cudaMalloc(&mr_[c], sizeof(double) * op.nodes));
+    CG_CUDA(cudaMalloc(&mp_[c], sizeof(double) * op.nodes));
+    CG_CUDA(cudaMalloc(&mw_[c], sizeof(double) * op.nodes));
+  }
+  if (count > mcount_) {
+    mcount_ = count;
+    if (mexec_) cudaGraphExecDestroy(mexec_);
+    mexec_ = nullptr;
+  }
+  if (!msc_) {
+    CG_CUDA(cudaMalloc(&msc_, sizeof(CgScalars) * kMaxComp));
+    CG_CUDA(cudaMemset(msc_, 0, sizeof(CgScalars) * kMaxComp));
+    CG_CUDA(cudaMallocHost(&mhsc_, sizeof(CgScalars) * kMaxComp));
+    CG_CUDA(cudaMalloc(&mflag_, sizeof(int) * kMaxComp));
+    CG_CUDA(cudaMalloc(&mprm_, sizeof(CgParams) * kMaxComp));
+    CG_CUDA(cudaMallocHost(&mhprm_, sizeof(CgParams) * kMaxComp));
+    CG_CUDA(cudaMalloc(&dmulti_, sizeof(CgMulti)));
+  }
+  const int64_t stride = 4 * std::max<int64_t>(std::max(k1_blocks(op), k2_blocks(op)), 2048);
+  if (mstride_ < stride) {
+    cudaFree(mpart_);
+    CG_CUDA(cudaMalloc(&mpart_, sizeof(double) * stride * kMaxComp));
+    mstride_ = stride;
+    if (mexec_) cudaGraphExecDestroy(mexec_);
+    mexec_ = nullptr;
+  }
+  if (mhist_len_ < (int64_t)run.max_it + 1) {
+    for (int c = 0; c < kMaxComp; ++c) cudaFree(mhist_[c]);
+    mhist_len_ = (int64_t)run.max_it + 1;
+    for (int c = 0; c < kMaxComp; ++c)
+      CG_CUDA(cudaMalloc(&mhist_[c], sizeof(double) * mhist_len_));
+    if (mexec_) cudaGraphExecDestroy(mexec_);
+    mexec_ = nullptr;
+  }
+  return SBX_OK;
+}
+
+// [per component: continuity check of b, w = mask gs(A x0), prologue] ->
+// WHILE {kUnroll x (K1, K2) over all components} -> per component x += alpha p
+int CgEngine::build_multi_graph(const CgRun* runs, int count) {
+  const CgRun& run = runs[0];
+  const OpDev& op = *run.op;
+  const int64_t N = op.nodes;
+  cudaStream_t s = run.stream;
+  CgMulti hm{};
+  hm.ncomp = count;
+  for (int c = 0; c < count; ++c) {
+    hm.r[c] = mr_[c];
+    hm.p[c] = mp_[c];
+    hm.x[c] = runs[c].x;
+    hm.w[c] = mw_[c];
+    hm.sc[c] = msc_ + c;
+    hm.hist[c] = mhist_[c];
+  }
+  hm.part_stride = mstride_;
+  CG_CUDA(cudaMemcpyAsync(dmulti_, &hm, sizeof(hm), cudaMemcpyHostToDevice, s));
+  CG_CUDA(cudaStreamSynchronize(s));
+  if (mexec_) cudaGraphExecDestroy(mexec_);
+  if (mgraph_) cudaGraphDestroy(mgraph_);
+  mexec_ = nullptr;
+  mgraph_ = nullptr;
+  CG_CUDA(cudaGraphCreate(&mgraph_, 0));
+  cudaGraph_t pre = nullptr;
+  CG_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+  cudaError_t ep = cudaSuccess;
+  for (int c = 0; c < count && ep == cudaSuccess; ++c) {
+    cudaMemsetAsync(mflag_ + c, 0, sizeof(int), s);
+    cudaMemsetAsync(&msc_[c].pre, 0, sizeof(int32_t), s);
+    if (op.lat)
+      ep = launch_check_rhs_box(op, runs[c].b, mflag_ + c, s);
+    else if (op.nB > 0)
+      cg_check_rhs_kernel<<<(unsigned)((op.nB + 255) / 256), 256, 0, s>>>(
+          op.b_off, op.b_idx, op.nB, runs[c].b, mflag_ + c);
+    if (ep == cudaSuccess)
+      ep = launch_axhelm(op, runs[c].x, mw_[c], run.h1, run.h2, false, false, s);
+    if (ep == cudaSuccess) ep = launch_gs(op, mw_[c], true, s);
+    int64_t blocks = std::min<int64_t>((N + 1023) / 1024, 1184);
+    if (blocks < 1) blocks = 1;
+    cg_prologue_kernel<<<(unsigned)blocks, 256, 0, s>>>(
+        N, runs[c].b, nullptr, mw_[c], run.dinv, op.inv_mult, mr_[c], mpart_ + c * mstride_,
+        msc_ + c, mprm_ + c, mhist_[c], mflag_ + c);
+    if (ep == cudaSuccess) ep = cudaGetLastError();
+  }
+  CG_CUDA(cudaStreamEndCapture(s, &pre));
+  CG_CUDA(ep);
+  cudaGraphNode_t npre, nloop, npost;
+  CG_CUDA(cudaGraphAddChildGraphNode(&npre, mgraph_, nullptr, 0, pre));
+  cudaGraphDestroy(pre);
+  cudaGraphConditionalHandle handle;
+  CG_CUDA(cudaGraphConditionalHandleCreate(&handle, mgraph_, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams params = {};
+  params.type = cudaGraphNodeTypeConditional;
+  params.conditional.handle = handle;
+  params.conditional.type = cudaGraphCondTypeWhile;
+  params.conditional.size = 1;
+  CG_CUDA(cudaGraphAddNode(&nloop, mgraph_, &npre, 1, &params));
+  cudaGraph_t body = params.conditional.phGraph_out[0];
+  CG_CUDA(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0,
+                                        cudaStreamCaptureModeRelaxed));
+  t_multi = dmulti_;
+  t_ncomp = count;
+  const int unroll = cg_unroll();
+  cudaError_t e1 = cudaSuccess, e2 = cudaSuccess;
+  for (int u = 0; u < unroll && e1 == cudaSuccess && e2 == cudaSuccess; ++u) {
+    e1 = k1(op, mr_[0], run.dinv, mp_[0], runs[0].x, mw_[0], run.h1, run.h2, msc_, mpart_, s);
+    e2 = k2(op, mw_[0], mr_[0], run.dinv, msc_, mpart_, mhist_[0], mhist_len_, handle, 1, s);
+  }
+  t_multi = nullptr;
+  t_ncomp = 1;
+  cudaGraph_t captured = nullptr;
+  const cudaError_t e3 = cudaStreamEndCapture(s, &captured);
+  if (e1 == cudaErrorNotSupported || e2 == cudaErrorNotSupported) {
+    cudaGetLastError();
+    return kCgFallback;  // no pipelined kernels for this context: solve one by one
+  }
+  CG_CUDA(e1);
+  CG_CUDA(e2);
+  CG_CUDA(e3);
+  cudaGraph_t post = nullptr;
+  CG_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+  for (int c = 0; c < count; ++c)
+    cg_finish_kernel<<<(unsigned)std::min<int64_t>((N + 255) / 256, 148 * 16), 256, 0, s>>>(
+        N, mp_[c], runs[c].x, msc_ + c);
+  const cudaError_t ef = cudaGetLastError();
+  CG_CUDA(cudaStreamEndCapture(s, &post));
+  CG_CUDA(ef);
+  CG_CUDA(cudaGraphAddChildGraphNode(&npost, mgraph_, &nloop, 1, post));
+  cudaGraphDestroy(post);
+  CG_CUDA(cudaGraphInstantiate(&mexec_, mgraph_, 0));
+  for (int c = 0; c < kMaxComp; ++c) {
+    mkey_[2 * c] = c < count ? runs[c].x : nullptr;
+    mkey_[2 * c + 1] = c < count ? runs[c].b : nullptr;
+  }
+  mkey_[2 * kMaxComp] = run.op;
+  mkey_[2 * kMaxComp + 1] = run.dinv;
+  mkey_[2 * kMaxComp + 2] = run.stream;
+  mkey_[2 * kMaxComp + 3] = reinterpret_cast<const void*>((intptr_t)count);
+  mkey_h_[0] = run.h1;
+  mkey_h_[1] = run.h2;
+  return SBX_OK;
+}
+
+int CgEngine::solve_multi(const CgRun* runs, int count, sbx_pcg_result* res) {
+  if (count < 1 || count > kMaxComp) {
+    err_ = "solve_multi: 1 to 3 right-hand sides";
+    return SBX_E_INVALID;
+  }
+  const CgRun& run = runs[0];
+  const OpDev& op = *run.op;
+  if (!run.interior_clean || op.n < 2 || op.n > 16 || run.dist || !op.box) return kCgFallback;
+  for (int c = 0; c < count; ++c)
+    if (!aligned16(runs[c].x) || !aligned16(runs[c].b)) return kCgFallback;
+  if (ensure_multi(run, count) != SBX_OK) return SBX_E_CUDA;
+  cudaStream_t s = run.stream;
+  bool same = mexec_ != nullptr && mkey_[2 * kMaxComp] == run.op &&
+              mkey_[2 * kMaxComp + 1] == run.dinv && mkey_[2 * kMaxComp + 2] == run.stream &&
+              mkey_[2 * kMaxComp + 3] == reinterpret_cast<const void*>((intptr_t)count) &&
+              mkey_h_[0] == run.h1 && mkey_h_[1] == run.h2;
+  for (int c = 0; c < count && same; ++c)
+    same = mkey_[2 * c] == runs[c].x && mkey_[2 * c + 1] == runs[c].b;
+  if (!same) {
+    const int rc = build_multi_graph(runs, count);
+    if (rc != SBX_OK) return rc;
+  }
+  for (int c = 0; c < count; ++c) {
+    mhprm_[c].tol = runs[c].tol;
+    mhprm_[c].max_it = runs[c].max_it;
+  }
+  CG_CUDA(cudaMemcpyAsync(mprm_, mhprm_, sizeof(CgParams) * count, cudaMemcpyHostToDevice, s));
+  CG_CUDA(cudaGraphLaunch(mexec_, s));
+  CG_CUDA(cudaMemcpyAsync(mhsc_, msc_, sizeof(CgScalars) * count, cudaMemcpyDeviceToHost, s));
+  CG_CUDA(cudaStreamSynchronize(s));
+  for (int c = 0; c < count; ++c)
+    if (mhsc_[c].pre & kPreRhsBad) return kCgFallback;  // nothing was written
+  int worst = SBX_OK;
+  for (int c = 0; c < count; ++c) {
+    std::memset(&res[c], 0, sizeof(res[c]));
+    res[c].error_iteration = -1;
+    if (mhsc_[c].pre & kPreZeroRhs) {
+      CG_CUDA(cudaMemsetAsync(runs[c].x, 0, sizeof(double) * op.nodes, s));
+      res[c].converged = 1;
+      continue;
+    }
+    const int rc = collect_from(mhsc_[c], mhist_[c], runs[c], &res[c]);
+    if (rc != SBX_OK && worst == SBX_OK) worst = rc;
+  }
+  CG_CUDA(cudaStreamSynchronize(s));
+  return worst;
 }
 
 int CgEngine::run_timed_loop(const CgRun& run) {
@@ -1814,7 +2080,11 @@ int CgEngine::solve(const CgRun& run, sbx_pcg_result* res) {
 
 // Results of a finished solve from the scalars already copied to hsc_.
 int CgEngine::collect(const CgRun& run, sbx_pcg_result* res) {
-  const CgScalars& o = *hsc_;
+  return collect_from(*hsc_, hist_, run, res);
+}
+
+int CgEngine::collect_from(const CgScalars& o, const double* dhist, const CgRun& run,
+                           sbx_pcg_result* res) {
   res->iterations = o.it;
   res->converged = o.converged;
   res->rel_residual = o.rel;
@@ -1822,7 +2092,7 @@ int CgEngine::collect(const CgRun& run, sbx_pcg_result* res) {
   res->history_length = (int64_t)o.it + 1;
   if (run.history && run.history_capacity > 0) {
     const int64_t cnt = std::min<int64_t>(res->history_length, run.history_capacity);
-    CG_CUDA(cudaMemcpy(run.history, hist_, sizeof(double) * cnt, cudaMemcpyDeviceToHost));
+    CG_CUDA(cudaMemcpy(run.history, dhist, sizeof(double) * cnt, cudaMemcpyDeviceToHost));
   }
   if (o.status == 5 || o.status == 6) {
     res->error_iteration = o.err_it;

@@ -39,6 +39,11 @@ class CgEngine {
   int solve(const CgRun& run, sbx_pcg_result* res);
   const std::string& error() const { return err_; }
   int kernel_time(const char* name, double* total_ms, int64_t* launches) const;
+  // Batched solve of count <= kMaxComp right-hand sides with one operator
+  // (the velocity components of FlowSolver::solve_velocity_star): one graph,
+  // K1 / K2 with grid.y = component, each component's initial guess applied
+  // in the graph; per component the same arithmetic as solve().
+  int solve_multi(const CgRun* runs, int count, sbx_pcg_result* res);
   // Test hook: one launch of the solver's K1 in its first-iteration form
   // (p = r, no preconditioner, x untouched) on u, so w = A_local u comes out
   // of exactly the kernel (and metric variant) the solve runs.
@@ -51,6 +56,10 @@ class CgEngine {
   int build_solve_graph(const CgRun& run);
   int solve_graph(const CgRun& run, sbx_pcg_result* res, bool* general);
   int collect(const CgRun& run, sbx_pcg_result* res);
+  int collect_from(const CgScalars& o, const double* dhist, const CgRun& run,
+                   sbx_pcg_result* res);
+  int ensure_multi(const CgRun& run, int count);
+  int build_multi_graph(const CgRun* runs, int count);
   int run_timed_loop(const CgRun& run);
 
   const OpDev* op_ = nullptr;
@@ -72,6 +81,24 @@ class CgEngine {
   cudaGraph_t sgraph_ = nullptr;
   cudaGraphExec_t sexec_ = nullptr;
   bool have_sgraph_ = false;
+  // batched solves
+  const OpDev* mop_ = nullptr;
+  int mcount_ = 0;
+  double *mr_[kMaxComp] = {}, *mp_[kMaxComp] = {}, *mw_[kMaxComp] = {};
+  double* mhist_[kMaxComp] = {};
+  int64_t mhist_len_ = 0;
+  CgScalars* msc_ = nullptr;   // device [kMaxComp]
+  CgScalars* mhsc_ = nullptr;  // pinned
+  double* mpart_ = nullptr;
+  int64_t mstride_ = 0;
+  int* mflag_ = nullptr;       // rhs check per component
+  CgParams* mprm_ = nullptr;
+  CgParams* mhprm_ = nullptr;  // pinned
+  CgMulti* dmulti_ = nullptr;
+  cudaGraph_t mgraph_ = nullptr;
+  cudaGraphExec_t mexec_ = nullptr;
+  const void* mkey_[2 * kMaxComp + 4] = {};
+  double mkey_h_[2] = {0.0, 0.0};
   // graph cache
   cudaGraph_t graph_ = nullptr;
   cudaGraphExec_t exec_ = nullptr;

@@ -79,6 +79,27 @@ struct CgScalars {
   int32_t pad_;
   double mu;  // pressure CG: mean of r/diag (the deflated preconditioner)
 };
+// A batched solve of up to kMaxComp right-hand sides with one operator (the
+// three velocity components of FlowSolver::solve_velocity_star,
+// stepper.cpp:188-238): the fused kernels run with grid.y = component, every
+// component with its own vectors and scalars (device copy of this struct).
+constexpr int kMaxComp = 3;
+struct CgMulti {
+  int ncomp;
+  double* r[kMaxComp];
+  double* p[kMaxComp];
+  double* x[kMaxComp];
+  double* w[kMaxComp];
+  CgScalars* sc[kMaxComp];
+  double* hist[kMaxComp];
+  int64_t part_stride;  // partials per component
+};
+// any component still iterating (the batched loop's WHILE condition)
+__device__ __forceinline__ bool multi_active(const CgMulti* m) {
+  bool a = false;
+  for (int c = 0; c < m->ncomp; ++c) a |= (*(const volatile int32_t*)&m->sc[c]->done) == 0;
+  return a;
+}
 // CgScalars::pre
 constexpr int kPreNonzeroX = 1;  // x0 != 0: r = b - A x0 needs the general path
 constexpr int kPreRhsBad = 2;    // b not continuous / not masked: EXACT fallback

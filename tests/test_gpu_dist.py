@@ -39,6 +39,12 @@ def test_dist_check_8_ranks_oversubscribed(cuda):
     pair at the largest supported world size."""
     if cuda.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
+    if not os.environ.get("SBX_TEST_OVERSUB"):
+        # several ranks per GPU run spin-waiting exchange kernels as separate
+        # processes on one device: nothing guarantees they are co-scheduled
+        # (B200 driver 580 raised context-switch timeouts for such setups), so
+        # this case runs only on request
+        pytest.skip("set SBX_TEST_OVERSUB=1 to run ranks oversubscribed on the GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=8",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
            os.path.join(ROOT, "tools", "dist_check.py")]
