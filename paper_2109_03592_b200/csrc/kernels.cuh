@@ -227,6 +227,7 @@ struct PresDev {
   int64_t E = 0, Np = 0;  // elements, pressure nodes E*m^3
   const double* tl = nullptr;
   const double* mats = nullptr;
+  const double* hmats = nullptr;  // host copy (kernel-parameter operators)
 };
 cudaError_t launch_p_grad(const PresDev& P, const double* p, double* const g[3], cudaStream_t s);
 cudaError_t launch_p_div(const PresDev& P, const double* const v[3], double* q, cudaStream_t s);

@@ -368,6 +368,307 @@ __global__ void __launch_bounds__(kPThreads)
   }
 }
 
+// ---- pencil kernels (n <= 10): each thread owns a 1-D pencil of a pass, its
+// inputs in registers, the 1-D operator as compile-time constant-bank operands
+// (kernel parameters), every component of a pass in flight at once
+// (CP = 3) or one component per pass (CP = 1, less shared memory).
+template <int n>
+struct PMatK {
+  static constexpr int m = n - 2;
+  double It[n * m], Ct[n * m];  // I^T, (I D)^T   [n][m]
+  double I[m * n], CI[m * n];   // I, I D         [m][n]
+  double w[m], x[m];            // GL weights, nodes
+};
+
+template <int n, int CP>
+struct PGrad2 {
+  static constexpr int m = n - 2, m2 = m * m, m3 = m2 * m;
+  static constexpr int F_D = 9 * m3, P_D = m3, A_D = 3 * CP * n * m2, B_D = 2 * CP * n * n * m;
+  static constexpr size_t bytes = sizeof(double) * (F_D + P_D + A_D + B_D);
+};
+
+template <int n, int CP, bool CG>
+__global__ void __launch_bounds__(128)
+    p_grad2_kernel(const double* __restrict__ pin, int64_t E, const double* __restrict__ TL,
+                   PMatK<n> M, double* __restrict__ g0, double* __restrict__ g1,
+                   double* __restrict__ g2, PCgArgs cg) {
+  using S = PGrad2<n, CP>;
+  constexpr int m = n - 2, m2 = m * m, m3 = m2 * m, n3 = n * n * n;
+  extern __shared__ double psm[];
+  double* sF = psm;          // [9][m3]: F[pd*3 + comp]
+  double* sp = sF + S::F_D;  // [m3]
+  double* sA = sp + S::P_D;  // [CP][3][n][m][m]  (kz, jj, ii)
+  double* sB = sA + S::A_D;  // [CP][2][n][n][m]  (kz, jy, ii)
+  if (CG && cg.sc->done) return;
+  double beta = 0.0, ap = 0.0, mu = 0.0;
+  int first = 1;
+  if constexpr (CG) {
+    beta = cg.sc->beta;
+    ap = cg.sc->alpha_prev;
+    mu = cg.sc->mu;
+    first = cg.sc->first;
+  }
+  double* outs[3] = {g0, g1, g2};
+  for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
+    __syncthreads();
+    for (int q = threadIdx.x; q < m3; q += blockDim.x) {
+      double F[9];
+      gl_metric(TL + e * 24, M.x, M.w, q % m, (q / m) % m, q / m2, F);
+#pragma unroll
+      for (int c = 0; c < 9; ++c) sF[c * m3 + q] = F[c];
+      const int64_t a = e * m3 + q;
+      double pv;
+      if constexpr (CG) {
+        const double rv = cg.r[a];
+        const double z = (cg.dinv ? rv * cg.dinv[a] : rv) - mu;
+        pv = z;
+        if (!first) {
+          const double po = cg.p[a];
+          pv = fma(beta, po, z);
+          cg.x[a] = fma(ap, po, cg.x[a]);
+        }
+        cg.p[a] = pv;
+      } else {
+        pv = pin[a];
+      }
+      sp[q] = pv;
+    }
+    for (int c0 = 0; c0 < 3; c0 += CP) {
+      __syncthreads();
+      // z pass: pencil (jj, ii) of field (comp, pd): A = Mz t, Mz = Ct (pd = 2) or It
+      for (int job = threadIdx.x; job < CP * 3 * m2; job += blockDim.x) {
+        const int cl = job / (3 * m2), pd = (job / m2) % 3, jjii = job % m2;
+        const int comp = c0 + cl;
+        double t[m];
+#pragma unroll
+        for (int kk = 0; kk < m; ++kk)
+          t[kk] = sF[(pd * 3 + comp) * m3 + kk * m2 + jjii] * sp[kk * m2 + jjii];
+        double* A = sA + (cl * 3 + pd) * n * m2 + jjii;
+        if (pd == 2) {
+#pragma unroll
+          for (int kz = 0; kz < n; ++kz) {
+            double acc = 0.0;
+#pragma unroll
+            for (int kk = 0; kk < m; ++kk) acc = fma(M.Ct[kz * m + kk], t[kk], acc);
+            A[kz * m2] = acc;
+          }
+        } else {
+#pragma unroll
+          for (int kz = 0; kz < n; ++kz) {
+            double acc = 0.0;
+#pragma unroll
+            for (int kk = 0; kk < m; ++kk) acc = fma(M.It[kz * m + kk], t[kk], acc);
+            A[kz * m2] = acc;
+          }
+        }
+      }
+      __syncthreads();
+      // y pass: pencil (kz, ii): B0 = Iy A0, B12 = Cy A1 + Iy A2
+      for (int job = threadIdx.x; job < CP * n * m; job += blockDim.x) {
+        const int cl = job / (n * m), kz = (job / m) % n, ii = job % m;
+        const double* A = sA + cl * 3 * n * m2 + kz * m2 + ii;
+        double a0[m], a1[m], a2[m];
+#pragma unroll
+        for (int jj = 0; jj < m; ++jj) {
+          a0[jj] = A[jj * m];
+          a1[jj] = A[n * m2 + jj * m];
+          a2[jj] = A[2 * n * m2 + jj * m];
+        }
+        double* B = sB + cl * 2 * n * n * m + kz * n * m + ii;
+#pragma unroll
+        for (int jy = 0; jy < n; ++jy) {
+          double b0 = 0.0, b12 = 0.0;
+#pragma unroll
+          for (int jj = 0; jj < m; ++jj) {
+            b0 = fma(M.It[jy * m + jj], a0[jj], b0);
+            b12 = fma(M.Ct[jy * m + jj], a1[jj], b12);
+            b12 = fma(M.It[jy * m + jj], a2[jj], b12);
+          }
+          B[jy * m] = b0;
+          B[n * n * m + jy * m] = b12;
+        }
+      }
+      __syncthreads();
+      // x pass: pencil (kz, jy): g = Cx B0 + Ix B12, a row of n outputs
+      for (int job = threadIdx.x; job < CP * n * n; job += blockDim.x) {
+        const int cl = job / (n * n), row = job % (n * n);
+        const double* B = sB + cl * 2 * n * n * m + row * m;
+        double b0[m], b12[m];
+#pragma unroll
+        for (int ii = 0; ii < m; ++ii) {
+          b0[ii] = B[ii];
+          b12[ii] = B[n * n * m + ii];
+        }
+        double* out = outs[c0 + cl] + e * n3 + row * n;
+#pragma unroll
+        for (int ix = 0; ix < n; ++ix) {
+          double acc = 0.0;
+#pragma unroll
+          for (int ii = 0; ii < m; ++ii) {
+            acc = fma(M.Ct[ix * m + ii], b0[ii], acc);
+            acc = fma(M.It[ix * m + ii], b12[ii], acc);
+          }
+          out[ix] = acc;
+        }
+      }
+    }
+  }
+}
+
+template <int n, int CP>
+struct PDiv2 {
+  static constexpr int m = n - 2, m2 = m * m, m3 = m2 * m, n3 = n * n * n;
+  static constexpr int F_D = 9 * m3, V_D = 3 * n3, X_D = 2 * CP * n * n * m,
+                       Y_D = 3 * CP * n * m2, Q_D = 3 * m3;
+  static constexpr size_t bytes = sizeof(double) * (F_D + V_D + X_D + Y_D + Q_D);
+};
+
+template <int n, int CP, bool CG>
+__global__ void __launch_bounds__(128)
+    p_div2_kernel(const double* __restrict__ v0, const double* __restrict__ v1,
+                  const double* __restrict__ v2, int64_t E, const double* __restrict__ TL,
+                  PMatK<n> M, double* __restrict__ qout, const double* __restrict__ pdot,
+                  double* __restrict__ partials, CgScalars* __restrict__ sc) {
+  using S = PDiv2<n, CP>;
+  constexpr int m = n - 2, m2 = m * m, m3 = m2 * m, n3 = n * n * n;
+  extern __shared__ double psm[];
+  __shared__ double red[32];
+  __shared__ bool is_last;
+  double* sF = psm;          // [9][m3]
+  double* sV = sF + S::F_D;  // [3][n3]
+  double* sX = sV + S::V_D;  // [CP][2][n][n][m]   (k, j, a)
+  double* sY = sX + S::X_D;  // [CP][3][n][m][m]   (k, b, a)
+  double* sQ = sY + S::Y_D;  // [3][m3] per-component contributions
+  if (CG && sc->done) return;
+  const double* ins[3] = {v0, v1, v2};
+  double pq = 0.0;
+  for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
+    __syncthreads();
+    for (int q = threadIdx.x; q < m3; q += blockDim.x) {
+      double F[9];
+      gl_metric(TL + e * 24, M.x, M.w, q % m, (q / m) % m, q / m2, F);
+#pragma unroll
+      for (int c = 0; c < 9; ++c) sF[c * m3 + q] = F[c];
+    }
+    for (int q = threadIdx.x; q < 3 * n3; q += blockDim.x) sV[q] = ins[q / n3][e * n3 + q % n3];
+    for (int c0 = 0; c0 < 3; c0 += CP) {
+      __syncthreads();
+      // x pass: row (k, j) of component: X0 = CIx v, X12 = Ix v
+      for (int job = threadIdx.x; job < CP * n * n; job += blockDim.x) {
+        const int cl = job / (n * n), row = job % (n * n);
+        const double* v = sV + (c0 + cl) * n3 + row * n;
+        double vr[n];
+#pragma unroll
+        for (int i = 0; i < n; ++i) vr[i] = v[i];
+        double* X = sX + cl * 2 * n * n * m + row * m;
+#pragma unroll
+        for (int a = 0; a < m; ++a) {
+          double x0 = 0.0, x12 = 0.0;
+#pragma unroll
+          for (int i = 0; i < n; ++i) {
+            x0 = fma(M.CI[a * n + i], vr[i], x0);
+            x12 = fma(M.I[a * n + i], vr[i], x12);
+          }
+          X[a] = x0;
+          X[n * n * m + a] = x12;
+        }
+      }
+      __syncthreads();
+      // y pass: pencil (k, a): Y0 = Iy X0, Y1 = CIy X12, Y2 = Iy X12
+      for (int job = threadIdx.x; job < CP * n * m; job += blockDim.x) {
+        const int cl = job / (n * m), k = (job / m) % n, a = job % m;
+        const double* X = sX + cl * 2 * n * n * m + k * n * m + a;
+        double x0[n], x12[n];
+#pragma unroll
+        for (int j = 0; j < n; ++j) {
+          x0[j] = X[j * m];
+          x12[j] = X[n * n * m + j * m];
+        }
+        double* Y = sY + cl * 3 * n * m2 + k * m2 + a;
+#pragma unroll
+        for (int b = 0; b < m; ++b) {
+          double y0 = 0.0, y1 = 0.0, y2 = 0.0;
+#pragma unroll
+          for (int j = 0; j < n; ++j) {
+            y0 = fma(M.I[b * n + j], x0[j], y0);
+            y1 = fma(M.CI[b * n + j], x12[j], y1);
+            y2 = fma(M.I[b * n + j], x12[j], y2);
+          }
+          Y[b * m] = y0;
+          Y[n * m2 + b * m] = y1;
+          Y[2 * n * m2 + b * m] = y2;
+        }
+      }
+      __syncthreads();
+      // z pass: pencil (b, a) of component: R_p = Mz_p Y_p, times the metric
+      for (int job = threadIdx.x; job < CP * m2; job += blockDim.x) {
+        const int cl = job / m2, ba = job % m2, comp = c0 + cl;
+        const double* Y = sY + cl * 3 * n * m2 + ba;
+        double y0[n], y1[n], y2[n];
+#pragma unroll
+        for (int k = 0; k < n; ++k) {
+          y0[k] = Y[k * m2];
+          y1[k] = Y[n * m2 + k * m2];
+          y2[k] = Y[2 * n * m2 + k * m2];
+        }
+#pragma unroll
+        for (int c = 0; c < m; ++c) {
+          double r0 = 0.0, r1 = 0.0, r2 = 0.0;
+#pragma unroll
+          for (int k = 0; k < n; ++k) {
+            r0 = fma(M.I[c * n + k], y0[k], r0);
+            r1 = fma(M.I[c * n + k], y1[k], r1);
+            r2 = fma(M.CI[c * n + k], y2[k], r2);
+          }
+          const int q = c * m2 + ba;
+          sQ[comp * m3 + q] = fma(sF[(0 * 3 + comp) * m3 + q], r0,
+                                  fma(sF[(1 * 3 + comp) * m3 + q], r1,
+                                      sF[(2 * 3 + comp) * m3 + q] * r2));
+        }
+      }
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < m3; q += blockDim.x) {
+      const double v = (sQ[q] + sQ[m3 + q]) + sQ[2 * m3 + q];
+      const int64_t a = e * m3 + q;
+      qout[a] = v;
+      if (CG) pq = fma(pdot[a], v, pq);
+    }
+  }
+  if constexpr (CG) {
+    double v = pq;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    if (wid == 0)
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) partials[blockIdx.x] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      is_last = atomicAdd(&sc->counter[0], 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!is_last || threadIdx.x != 0) return;
+    __threadfence();
+    double tot = 0.0;
+    for (int b = 0; b < (int)gridDim.x; ++b) tot += partials[b];
+    sc->counter[0] = 0;
+    sc->pq = tot;
+    if (!isfinite(tot) || tot <= 0.0) {
+      sc->status = 5;
+      sc->err_it = sc->it;
+      sc->done = 1;
+    } else {
+      sc->alpha = sc->rz / tot;
+    }
+  }
+}
+
 // pressure_operator_diagonal (stepper.cpp:250-275) in closed form: the
 // gradient of the unit vector at GL node q restricted to its element is
 // g_comp(a) = sum_pd F[pd][comp](q) prod_dir M_{pd,dir}[a_dir][q_dir]
@@ -566,11 +867,52 @@ unsigned pgrid(int64_t E) {
   return (unsigned)(g < 1 ? 1 : g);
 }
 
+// the pencil kernels' 1-D operators as a kernel parameter (constant bank)
+template <int n>
+PMatK<n> pmatk(const PresDev& P) {
+  constexpr int m = n - 2;
+  PMatK<n> M;
+  const double* h = P.hmats;
+  for (int q = 0; q < n * m; ++q) {
+    M.It[q] = h[PMat<n>::OFF_IT + q];
+    M.Ct[q] = h[PMat<n>::OFF_CT + q];
+    M.I[q] = h[PMat<n>::OFF_I + q];
+    M.CI[q] = h[PMat<n>::OFF_CI + q];
+  }
+  for (int q = 0; q < m; ++q) {
+    M.w[q] = h[PMat<n>::OFF_W + q];
+    M.x[q] = h[PMat<n>::OFF_X + q];
+  }
+  return M;
+}
+
+// components per pass of the pencil kernels (all three while they fit)
+template <int n>
+constexpr int pencil_cp() {
+  return PGrad2<n, 3>::bytes <= 64 * 1024 && PDiv2<n, 3>::bytes <= 96 * 1024 ? 3 : 1;
+}
+
 template <int n>
 cudaError_t grad_t(const PresDev& P, const double* p, double* const g[3], const PCgArgs* cg,
                    cudaStream_t s) {
   if constexpr (n < 4) {
     return cudaErrorInvalidValue;
+  } else if constexpr (n <= 10) {
+    constexpr int CP = pencil_cp<n>();
+    const size_t sm = PGrad2<n, CP>::bytes;
+    const PMatK<n> M = pmatk<n>(P);
+    if (cg) {
+      cudaError_t e = set_smem(p_grad2_kernel<n, CP, true>, sm);
+      if (e != cudaSuccess) return e;
+      p_grad2_kernel<n, CP, true><<<pgrid(P.E), 128, sm, s>>>(nullptr, P.E, P.tl, M, g[0], g[1],
+                                                              g[2], *cg);
+    } else {
+      cudaError_t e = set_smem(p_grad2_kernel<n, CP, false>, sm);
+      if (e != cudaSuccess) return e;
+      p_grad2_kernel<n, CP, false><<<pgrid(P.E), 128, sm, s>>>(p, P.E, P.tl, M, g[0], g[1],
+                                                               g[2], PCgArgs{});
+    }
+    return cudaGetLastError();
   } else {
     const size_t sm = PGradSmem<n>::bytes;
     if (cg) {
@@ -593,6 +935,22 @@ cudaError_t div_t(const PresDev& P, const double* const v[3], double* q, const d
                   double* partials, CgScalars* sc, cudaStream_t s) {
   if constexpr (n < 4) {
     return cudaErrorInvalidValue;
+  } else if constexpr (n <= 10) {
+    constexpr int CP = pencil_cp<n>();
+    const size_t sm = PDiv2<n, CP>::bytes;
+    const PMatK<n> M = pmatk<n>(P);
+    if (sc) {
+      cudaError_t e = set_smem(p_div2_kernel<n, CP, true>, sm);
+      if (e != cudaSuccess) return e;
+      p_div2_kernel<n, CP, true><<<pgrid(P.E), 128, sm, s>>>(v[0], v[1], v[2], P.E, P.tl, M, q,
+                                                             pdot, partials, sc);
+    } else {
+      cudaError_t e = set_smem(p_div2_kernel<n, CP, false>, sm);
+      if (e != cudaSuccess) return e;
+      p_div2_kernel<n, CP, false><<<pgrid(P.E), 128, sm, s>>>(v[0], v[1], v[2], P.E, P.tl, M, q,
+                                                              nullptr, nullptr, nullptr);
+    }
+    return cudaGetLastError();
   } else {
     const size_t sm = PDivSmem<n>::bytes;
     if (sc) {
@@ -844,6 +1202,8 @@ int PressureEngine::setup(const OpDev& op, cudaStream_t s) {
   PE_CUDA(cudaMemcpyAsync(mats_, mats.data(), sizeof(double) * mats.size(),
                           cudaMemcpyHostToDevice, s));
   P_.mats = mats_;
+  hmats_ = mats;
+  P_.hmats = hmats_.data();
   // inv_bdiag = mask / gs_sum(bm)   (FlowSolver constructor, stepper.cpp:79-84)
   if (!op.bm) {
     err_ = "pressure operator: needs the mass factors (bm)";

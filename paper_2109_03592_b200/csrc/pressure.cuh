@@ -56,6 +56,7 @@ class PressureEngine {
   PresDev P_;
   bool ready_ = false;
   double* mats_ = nullptr;
+  std::vector<double> hmats_;
   PresExact X_;
   double* xmats_ = nullptr;   // d | iv | ivt | glx | glw (EXACT kernels)
   double* pdiag_x_ = nullptr;

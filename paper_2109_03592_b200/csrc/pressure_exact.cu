@@ -287,53 +287,65 @@ __global__ void __launch_bounds__(kXThreads)
                   double* __restrict__ o1, double* __restrict__ o2) {
   const int n3 = n * n * n;
   extern __shared__ double xs[];
-  double* in = xs;
+  double* in = xs;         // u0 | u1 | u2 of the element
+  double* sD = in + 3 * n3;
+  double* sX = sD + n * n;
+  double* scr = sX + n;    // the element's 24 corner coordinates
   const double* us[3] = {u0, u1, u2};
   double* outs[3] = {o0, o1, o2};
+  for (int q = threadIdx.x; q < n * n; q += blockDim.x) sD[q] = D[q];
+  for (int q = threadIdx.x; q < n; q += blockDim.x) sX[q] = gllx[q];
   for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
-    for (int comp = 0; comp < 3; ++comp) {
-      __syncthreads();
-      for (int q = threadIdx.x; q < n3; q += blockDim.x) in[q] = us[comp][e * n3 + q];
-      __syncthreads();
-      for (int q = threadIdx.x; q < n3; q += blockDim.x) {
-        const int i = q % n, j = (q / n) % n, k = q / (n * n);
+    __syncthreads();
+    for (int q = threadIdx.x; q < 3 * n3; q += blockDim.x)
+      in[q] = us[q / n3][e * n3 + q % n3];
+    if (threadIdx.x < 24) scr[threadIdx.x] = corners[e * 24 + threadIdx.x];
+    __syncthreads();
+    for (int q = threadIdx.x; q < n3; q += blockDim.x) {
+      const int i = q % n, j = (q / n) % n, k = q / (n * n);
+      // drdx at GLL node (i, j, k): inv3 of the TrilinearMap Jacobian, once
+      // per node for the three components
+      const double r = sX[i], s = sX[j], t = sX[k];
+      const double sh[3][2] = {{0.5 * (1 - r), 0.5 * (1 + r)},
+                               {0.5 * (1 - s), 0.5 * (1 + s)},
+                               {0.5 * (1 - t), 0.5 * (1 + t)}};
+      double J[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        const int b0 = v & 1, b1 = (v >> 1) & 1, b2 = (v >> 2) & 1;
+        const double d0 = b0 ? 0.5 : -0.5, d1 = b1 ? 0.5 : -0.5, d2 = b2 ? 0.5 : -0.5;
+        const double gr[3] = {d0 * sh[1][b1] * sh[2][b2], sh[0][b0] * d1 * sh[2][b2],
+                              sh[0][b0] * sh[1][b1] * d2};
+#pragma unroll
+        for (int p = 0; p < 3; ++p) {
+          const double xp = scr[v * 3 + p];
+          J[p * 3 + 0] += xp * gr[0];
+          J[p * 3 + 1] += xp * gr[1];
+          J[p * 3 + 2] += xp * gr[2];
+        }
+      }
+      const double det = J[0] * (J[4] * J[8] - J[5] * J[7]) -
+                         J[1] * (J[3] * J[8] - J[5] * J[6]) + J[2] * (J[3] * J[7] - J[4] * J[6]);
+      const double id = 1.0 / det;
+      const double R[9] = {(J[4] * J[8] - J[5] * J[7]) * id, (J[2] * J[7] - J[1] * J[8]) * id,
+                           (J[1] * J[5] - J[2] * J[4]) * id, (J[5] * J[6] - J[3] * J[8]) * id,
+                           (J[0] * J[8] - J[2] * J[6]) * id, (J[2] * J[3] - J[0] * J[5]) * id,
+                           (J[3] * J[7] - J[4] * J[6]) * id, (J[1] * J[6] - J[0] * J[7]) * id,
+                           (J[0] * J[4] - J[1] * J[3]) * id};
+      const int64_t a = e * n3 + q;
+      const double cv0 = c0[a], cv1 = c1[a], cv2 = c2[a], b = bm[a];
+      for (int comp = 0; comp < 3; ++comp) {
+        const double* u = in + comp * n3;
         double dr = 0.0, ds = 0.0, dt = 0.0;
         for (int l = 0; l < n; ++l) {
-          dr += D[i * n + l] * in[(k * n + j) * n + l];
-          ds += D[j * n + l] * in[(k * n + l) * n + i];
-          dt += D[k * n + l] * in[(l * n + j) * n + i];
+          dr += sD[i * n + l] * u[(k * n + j) * n + l];
+          ds += sD[j * n + l] * u[(k * n + l) * n + i];
+          dt += sD[k * n + l] * u[(l * n + j) * n + i];
         }
-        // drdx at GLL node (i, j, k): inv3 of the TrilinearMap Jacobian
-        const double* cr = corners + e * 24;
-        const double r = gllx[i], s = gllx[j], t = gllx[k];
-        const double sh[3][2] = {{0.5 * (1 - r), 0.5 * (1 + r)},
-                                 {0.5 * (1 - s), 0.5 * (1 + s)},
-                                 {0.5 * (1 - t), 0.5 * (1 + t)}};
-        double J[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-        for (int v = 0; v < 8; ++v) {
-          const int b0 = v & 1, b1 = (v >> 1) & 1, b2 = (v >> 2) & 1;
-          const double d0 = b0 ? 0.5 : -0.5, d1 = b1 ? 0.5 : -0.5, d2 = b2 ? 0.5 : -0.5;
-          const double gr[3] = {d0 * sh[1][b1] * sh[2][b2], sh[0][b0] * d1 * sh[2][b2],
-                                sh[0][b0] * sh[1][b1] * d2};
-          for (int p = 0; p < 3; ++p) {
-            const double xp = cr[v * 3 + p];
-            J[p * 3 + 0] += xp * gr[0];
-            J[p * 3 + 1] += xp * gr[1];
-            J[p * 3 + 2] += xp * gr[2];
-          }
-        }
-        const double det = J[0] * (J[4] * J[8] - J[5] * J[7]) -
-                           J[1] * (J[3] * J[8] - J[5] * J[6]) + J[2] * (J[3] * J[7] - J[4] * J[6]);
-        const double id = 1.0 / det;
-        const double R[9] = {(J[4] * J[8] - J[5] * J[7]) * id, (J[2] * J[7] - J[1] * J[8]) * id,
-                             (J[1] * J[5] - J[2] * J[4]) * id, (J[5] * J[6] - J[3] * J[8]) * id,
-                             (J[0] * J[8] - J[2] * J[6]) * id, (J[2] * J[3] - J[0] * J[5]) * id,
-                             (J[3] * J[7] - J[4] * J[6]) * id, (J[1] * J[6] - J[0] * J[7]) * id,
-                             (J[0] * J[4] - J[1] * J[3]) * id};
         double g[3];
+#pragma unroll
         for (int qq = 0; qq < 3; ++qq) g[qq] = R[0 + qq] * dr + R[3 + qq] * ds + R[6 + qq] * dt;
-        const int64_t a = e * n3 + q;
-        outs[comp][a] = bm[a] * (c0[a] * g[0] + c1[a] * g[1] + c2[a] * g[2]);
+        outs[comp][a] = b * (cv0 * g[0] + cv1 * g[1] + cv2 * g[2]);
       }
     }
   }
@@ -382,7 +394,7 @@ cudaError_t launch_p_diag_exact(const PresExact& X, const double* inv_bdiag, dou
 cudaError_t launch_advect(int64_t E, int n, const double* corners, const double* D,
                           const double* gllx, const double* bm, const double* const u[3],
                           const double* const c[3], double* const out[3], cudaStream_t s) {
-  const size_t sm = sizeof(double) * (size_t)n * n * n;
+  const size_t sm = sizeof(double) * (3 * (size_t)n * n * n + (size_t)n * n + n + 24);
   cudaError_t e = cudaFuncSetAttribute(advect_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
