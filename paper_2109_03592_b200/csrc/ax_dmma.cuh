@@ -64,29 +64,39 @@ struct DmmaLayout {
   static constexpr int V_D = 512;
   static constexpr int SLOT_D = G_D + NV * V_D;
   static constexpr int S = GROUPS * SPG;
-  static constexpr size_t BAR_BYTES = 512;
+  static constexpr size_t BAR_BYTES = 1024;
   static constexpr int AUX_D = 64 + 16;  // D (row-major) and GLL x[8], w[8]
   static constexpr size_t smem = BAR_BYTES + sizeof(double) * (size_t)(AUX_D + S * SLOT_D);
   static constexpr int threads = GROUPS * 32 + 32;
   static_assert(NV >= 3, "the u / sr / ss tiles overlay three staged vectors");
 };
 
+#ifndef SBX_DMMA_SPG
+#define SBX_DMMA_SPG 2  // slots per consumer warp (A/B knob)
+#endif
+#ifndef SBX_DMMA_MAXG
+#define SBX_DMMA_MAXG 6  // consumer warps (A/B knob)
+#endif
+#ifndef SBX_CONS_SUSPEND
+#define SBX_CONS_SUSPEND 0  // consumers wait for their slot suspended (A/B knob)
+#endif
+
 template <int NV>
 struct DmmaChoice {
   static constexpr size_t BUDGET = 225 * 1024;
+  static constexpr int SPG = SBX_DMMA_SPG;
   // at most 6 consumer warps: each holds ~250 registers (two columns'
   // metric constants, the t-derivatives and the accumulators)
   static constexpr int pick() {
-    for (int g = 6; g >= 1; --g)
+    for (int g = SBX_DMMA_MAXG; g >= 1; --g)
       if (DmmaLayout<NV, 1, 1>::BAR_BYTES +
               sizeof(double) * (DmmaLayout<NV, 1, 1>::AUX_D +
-                                (size_t)2 * g * DmmaLayout<NV, 1, 1>::SLOT_D) <=
+                                (size_t)SPG * g * DmmaLayout<NV, 1, 1>::SLOT_D) <=
           BUDGET)
         return g;
     return 0;
   }
   static constexpr int GROUPS = pick();
-  static constexpr int SPG = 2;
   static constexpr bool ok = GROUPS >= 1;
 };
 
@@ -104,6 +114,7 @@ __global__ void __launch_bounds__(DmmaLayout<Pol::NV, GROUPS, SPG>::threads, 1)
   __shared__ double red_sm[32];
   __shared__ bool last_flag;
   typename Pol::Args args_l = args;
+  partials = Pol::partials_of(args, partials);
   if (!Pol::init(args_l)) return;
   uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
   uint64_t* empty = full + S;
@@ -121,10 +132,26 @@ __global__ void __launch_bounds__(DmmaLayout<Pol::NV, GROUPS, SPG>::threads, 1)
     }
     mbar_fence_init();
   }
-  for (int q = threadIdx.x; q < 64; q += blockDim.x) sD[q] = Dp.d[q];
-  for (int q = threadIdx.x; q < 8; q += blockDim.x) {
-    sQ[q] = Qp.x[q];
-    sQ[8 + q] = Qp.w[q];
+  // (compile-time indices only: a runtime index into a by-value kernel
+  // parameter makes the compiler copy it to local memory, and every later
+  // access -- the metric's Qp.x[k], Qp.w[k] -- becomes a local load)
+  if (threadIdx.x < 32) {
+    const int l = threadIdx.x;
+#pragma unroll
+    for (int q = 0; q < 64; q += 32) {
+      double v = 0.0;
+#pragma unroll
+      for (int t = 0; t < 32; ++t)
+        if (l == t) v = Dp.d[q + t];
+      sD[q + l] = v;
+    }
+    if (l == 0) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        sQ[q] = Qp.x[q];
+        sQ[8 + q] = Qp.w[q];
+      }
+    }
   }
   __syncthreads();
 
@@ -179,7 +206,10 @@ __global__ void __launch_bounds__(DmmaLayout<Pol::NV, GROUPS, SPG>::threads, 1)
     for (int64_t m = g; m < M; m += GROUPS) {
       const int s = (int)(m % S);
       const int64_t e = blockIdx.x + m * gridDim.x;
-      mbar_wait(&full[s], (uint32_t)((m / S) & 1));
+      if (SBX_CONS_SUSPEND)
+        mbar_wait_backoff(&full[s], (uint32_t)((m / S) & 1));
+      else
+        mbar_wait(&full[s], (uint32_t)((m / S) & 1));
       const int nsend = meta[s];
       double* slot = slots + s * L::SLOT_D;
       double* V = slot + L::G_D;

@@ -104,8 +104,11 @@ struct CgK1Pol {
     const int32_t* esend_off;
     int stored;  // this thread pushed halo values (fence before the ticket)
     const CgMulti* multi;  // batched solve: this CTA's component is blockIdx.y
-    int64_t part_off;
   };
+  // batched solve: this CTA's component's partials
+  __device__ static double* partials_of(const Args& a, double* partials) {
+    return a.multi ? partials + blockIdx.y * a.multi->part_stride : partials;
+  }
   __device__ static bool init(Args& a) {
     if (a.multi) {
       const int c = blockIdx.y;
@@ -114,7 +117,7 @@ struct CgK1Pol {
       a.x = a.multi->x[c];
       a.w = a.multi->w[c];
       a.sc = a.multi->sc[c];
-      a.part_off = c * a.multi->part_stride;
+      a.multi = nullptr;  // (dead from here on: no register held across the sweeps)
     }
     if (a.sc->done) return false;
     a.first = a.sc->first;
@@ -194,7 +197,6 @@ __device__ void CgK1Pol<HAS_DINV, HAS_BM>::finish(const Args& a, double red, dou
   // system scope once, here, before the CTA's ticket; the last CTA then
   // releases them with dist_release_phase0)
   if (a.stored) __threadfence_system();
-  partials += a.part_off;
   const double v = cta_sum(red, sh);
   if (threadIdx.x == 0) partials[blockIdx.x] = v;
   CgScalars* sc = a.sc;

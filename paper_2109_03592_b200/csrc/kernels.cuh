@@ -236,7 +236,7 @@ cudaError_t launch_p_diag(const PresDev& P, const double* inv_bdiag, double* dia
 // g_c := scale * gs_sum(g_c) for c = 0..2 (gather-scatter of the velocity-grid
 // gradient, then the masked inverse assembled mass; stepper.cpp:242-245)
 cudaError_t launch_gs3_scale(const OpDev& op, double* const g[3], const double* scale,
-                             cudaStream_t s);
+                             cudaStream_t s, double* const* out = nullptr);
 struct PIterArgs {
   const OpDev* op;
   const double* inv_bdiag;
@@ -246,6 +246,7 @@ struct PIterArgs {
   double* x;
   double* q;
   double* g[3];
+  double* v[3];  // scale * gs(g) (out of place)
   double* partials;
   CgScalars* sc;
   double* hist;

@@ -120,6 +120,7 @@ struct AxPol {
     double h2;
   };
   __device__ static bool init(Args&) { return true; }
+  __device__ static double* partials_of(const Args&, double* partials) { return partials; }
   __device__ static const int32_t* send_index(const Args&) { return nullptr; }
   __device__ static void element_done(Args&, int, int64_t, int, int, int, int, int) {}
   __device__ static const double* vec(const Args& a, int q) { return q == 0 ? a.u : a.bm; }

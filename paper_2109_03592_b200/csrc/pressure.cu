@@ -26,6 +26,7 @@
 #include "kernels.cuh"
 #include "pressure.cuh"
 #include "sbx_internal.h"
+#include "tma.cuh"
 
 #include <algorithm>
 #include <cstdlib>
@@ -518,7 +519,7 @@ __global__ void __launch_bounds__(128)
 template <int n, int CP>
 struct PDiv2 {
   static constexpr int m = n - 2, m2 = m * m, m3 = m2 * m, n3 = n * n * n;
-  static constexpr int F_D = 9 * m3, V_D = 3 * n3, X_D = 2 * CP * n * n * m,
+  static constexpr int F_D = 9 * m3, V_D = 2 * 3 * n3, X_D = 2 * CP * n * n * m,
                        Y_D = 3 * CP * n * m2, Q_D = 3 * m3;
   static constexpr size_t bytes = sizeof(double) * (F_D + V_D + X_D + Y_D + Q_D);
 };
@@ -534,23 +535,34 @@ __global__ void __launch_bounds__(128)
   extern __shared__ double psm[];
   __shared__ double red[32];
   __shared__ bool is_last;
-  double* sF = psm;          // [9][m3]
-  double* sV = sF + S::F_D;  // [3][n3]
-  double* sX = sV + S::V_D;  // [CP][2][n][n][m]   (k, j, a)
+  double* sF = psm;           // [9][m3]
+  double* sVb = sF + S::F_D;  // [2][3][n3]: this element's fields, the next one's in flight
+  double* sX = sVb + S::V_D;  // [CP][2][n][n][m]   (k, j, a)
   double* sY = sX + S::X_D;  // [CP][3][n][m][m]   (k, b, a)
   double* sQ = sY + S::Y_D;  // [3][m3] per-component contributions
   if (CG && sc->done) return;
   const double* ins[3] = {v0, v1, v2};
   double pq = 0.0;
-  for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
-    __syncthreads();
+  // the three fields of an element, copied asynchronously one element ahead
+  auto prefetch = [&](int64_t ee, double* dst) {
+    if (ee < E)
+      for (int q = threadIdx.x; q < 3 * n3; q += blockDim.x)
+        cp_async8(dst + q, ins[q / n3] + ee * n3 + q % n3, true);
+    cp_async_commit();
+  };
+  prefetch(blockIdx.x, sVb);
+  int buf = 0;
+  for (int64_t e = blockIdx.x; e < E; e += gridDim.x, buf ^= 1) {
+    __syncthreads();  // the previous element is done with the other buffer
+    prefetch(e + gridDim.x, sVb + (buf ^ 1) * 3 * n3);
     for (int q = threadIdx.x; q < m3; q += blockDim.x) {
       double F[9];
       gl_metric(TL + e * 24, M.x, M.w, q % m, (q / m) % m, q / m2, F);
 #pragma unroll
       for (int c = 0; c < 9; ++c) sF[c * m3 + q] = F[c];
     }
-    for (int q = threadIdx.x; q < 3 * n3; q += blockDim.x) sV[q] = ins[q / n3][e * n3 + q % n3];
+    cp_async_wait<1>();  // this element's fields have landed (the next may still fly)
+    double* sV = sVb + buf * 3 * n3;
     for (int c0 = 0; c0 < 3; c0 += CP) {
       __syncthreads();
       // x pass: row (k, j) of component: X0 = CIx v, X12 = Ix v
@@ -1040,9 +1052,9 @@ cudaError_t launch_p_iteration(const PresDev& P, const PIterArgs& A,
   SBX_P_SWITCH(P.n, CALLI)
 #undef CALLI
   if (err != cudaSuccess) return err;
-  err = launch_gs3_scale(*A.op, A.g, A.inv_bdiag, s);
+  err = launch_gs3_scale(*A.op, A.g, A.inv_bdiag, s, A.v);
   if (err != cudaSuccess) return err;
-#define CALLJ(NN) err = div_t<NN>(P, A.g, A.q, A.p, A.partials, A.sc, s)
+#define CALLJ(NN) err = div_t<NN>(P, A.v, A.q, A.p, A.partials, A.sc, s)
   SBX_P_SWITCH(P.n, CALLJ)
 #undef CALLJ
   if (err != cudaSuccess) return err;
@@ -1123,7 +1135,8 @@ PressureEngine::~PressureEngine() {
     cudaFree(e.second);
   }
   for (double* v : pool_) cudaFree(v);
-  for (double* v : {mats_, inv_bdiag_, pdiag_, pdinv_, g_[0], g_[1], g_[2], r_, p_, q_,
+  for (double* v : {mats_, inv_bdiag_, pdiag_, pdinv_, g_[0], g_[1], g_[2], v_[0], v_[1], v_[2],
+                    r_, p_, q_,
                     partials_, hist_, sums_, xmats_, pdiag_x_, zx_, scal_})
     cudaFree(v);
   cudaFree(counter_);
@@ -1226,7 +1239,10 @@ int PressureEngine::setup(const OpDev& op, cudaStream_t s) {
   PE_CUDA(cudaMemset(counter_, 0, 4 * sizeof(uint32_t)));
   PE_CUDA(cudaMalloc(&flag_, sizeof(int)));
   PE_CUDA(cudaMalloc(&partials_, sizeof(double) * 8 * 148 * 16));
-  for (int c = 0; c < 3; ++c) PE_CUDA(cudaMalloc(&g_[c], sizeof(double) * op.nodes));
+  for (int c = 0; c < 3; ++c) {
+    PE_CUDA(cudaMalloc(&g_[c], sizeof(double) * op.nodes));
+    PE_CUDA(cudaMalloc(&v_[c], sizeof(double) * op.nodes));
+  }
   ready_ = true;
   return SBX_OK;
 }
@@ -1252,8 +1268,8 @@ int PressureEngine::div(const double* const v[3], double* q, cudaStream_t s) {
 
 int PressureEngine::apply(const double* p, double* q, cudaStream_t s) {
   PE_CUDA(launch_p_grad(P_, p, g_, s));
-  PE_CUDA(launch_gs3_scale(*op_, g_, inv_bdiag_, s));
-  PE_CUDA(launch_p_div(P_, g_, q, s));
+  PE_CUDA(launch_gs3_scale(*op_, g_, inv_bdiag_, s, v_));
+  PE_CUDA(launch_p_div(P_, v_, q, s));
   return SBX_OK;
 }
 
@@ -1525,8 +1541,8 @@ int PressureEngine::build_graph(cudaStream_t s, double* x, const double* dinv) {
   cudaGraph_t body = params.conditional.phGraph_out[0];
   PE_CUDA(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0,
                                         cudaStreamCaptureModeRelaxed));
-  PIterArgs A{op_, inv_bdiag_, r_, dinv, p_, x, q_, {g_[0], g_[1], g_[2]}, partials_, sc_,
-              hist_, hist_len_};
+  PIterArgs A{op_, inv_bdiag_, r_, dinv, p_, x, q_, {g_[0], g_[1], g_[2]},
+              {v_[0], v_[1], v_[2]}, partials_, sc_, hist_, hist_len_};
   cudaError_t e = cudaSuccess;
   for (int u = 0; u < 2 && e == cudaSuccess; ++u) e = launch_p_iteration(P_, A, handle, 1, s);
   cudaGraph_t captured = nullptr;

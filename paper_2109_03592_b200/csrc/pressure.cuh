@@ -66,6 +66,7 @@ class PressureEngine {
   double* pdiag_ = nullptr;
   double* pdinv_ = nullptr;
   double* g_[3] = {};
+  double* v_[3] = {};
   double *r_ = nullptr, *p_ = nullptr, *q_ = nullptr, *partials_ = nullptr, *hist_ = nullptr;
   int64_t hist_len_ = 0;
   double* sums_ = nullptr;  // device [8]

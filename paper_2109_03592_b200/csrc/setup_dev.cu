@@ -277,6 +277,52 @@ __global__ void gs3_scale_box_kernel(BoxLat b, int n, int cols, double* __restri
   }
 }
 
+// Out of place: v_c = scale * gs_sum(g_c).  Every thread sums its own node's
+// copies (the same copies in the same reference order for every copy, so
+// every copy gets the same bits as the in-place kernel) -- no serial owner
+// loop, the partner loads of all copies in flight at once.
+__global__ void gs3_scale_box_oop_kernel(BoxLat b, int n, int cols,
+                                         const double* __restrict__ f0,
+                                         const double* __restrict__ f1,
+                                         const double* __restrict__ f2,
+                                         const double* __restrict__ scale,
+                                         double* __restrict__ v0, double* __restrict__ v1,
+                                         double* __restrict__ v2) {
+  const int N = n - 1, n3 = n * n * n;
+  for (int col = blockIdx.x * blockDim.x + threadIdx.x; col < cols;
+       col += gridDim.x * blockDim.x) {
+    const Col32 c = col_of(b, n, col);
+    const bool face = c.i == 0 || c.i == N || c.j == 0 || c.j == N;
+    for (int k = 0; k < n; ++k) {
+      const int a = c.e * n3 + (k * n + c.j) * n + c.i;
+      const double w = scale[a];
+      if (!face && k != 0 && k != N) {
+        v0[a] = __dmul_rn(f0[a], w);
+        v1[a] = __dmul_rn(f1[a], w);
+        v2[a] = __dmul_rn(f2[a], w);
+        continue;
+      }
+      int idx[8];
+      bool masked;
+      const int m = copies32(b, n, c, k, idx, masked);
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+      for (int q = 0; q < m; ++q) {
+        s0 = __dadd_rn(s0, f0[idx[q]]);
+        s1 = __dadd_rn(s1, f1[idx[q]]);
+        s2 = __dadd_rn(s2, f2[idx[q]]);
+      }
+      if (m == 1) {  // a singleton: gs leaves it alone (no 0.0 + x)
+        s0 = f0[a];
+        s1 = f1[a];
+        s2 = f2[a];
+      }
+      v0[a] = __dmul_rn(s0, w);
+      v1[a] = __dmul_rn(s1, w);
+      v2[a] = __dmul_rn(s2, w);
+    }
+  }
+}
+
 __global__ void mul3_kernel(int64_t N, double* __restrict__ f0, double* __restrict__ f1,
                             double* __restrict__ f2, const double* __restrict__ scale) {
   for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < N;
@@ -460,7 +506,21 @@ cudaError_t launch_validate_geom(const double* corners, int64_t E, int n, const 
 }
 
 cudaError_t launch_gs3_scale(const OpDev& op, double* const g[3], const double* scale,
-                             cudaStream_t s) {
+                             cudaStream_t s, double* const* out) {
+  if (op.lat && out) {
+    const int cols = (int)(op.E * op.n * op.n);
+    gs3_scale_box_oop_kernel<<<grid_for(cols), 256, 0, s>>>(box_lat(op), op.n, cols, g[0], g[1],
+                                                            g[2], scale, out[0], out[1], out[2]);
+    return cudaGetLastError();
+  }
+  if (out) {
+    for (int c = 0; c < 3; ++c) {
+      const cudaError_t e = cudaMemcpyAsync(out[c], g[c], sizeof(double) * op.nodes,
+                                            cudaMemcpyDeviceToDevice, s);
+      if (e != cudaSuccess) return e;
+    }
+    return launch_gs3_scale(op, out, scale, s, nullptr);
+  }
   if (op.lat) {
     const int cols = (int)(op.E * op.n * op.n);
     gs3_scale_box_kernel<<<grid_for(cols), 256, 0, s>>>(box_lat(op), op.n, cols, g[0], g[1],
