@@ -309,7 +309,13 @@ sbx_status sbx_dist_plan_array(const sbx_dist_plan* plan, int which, void* out);
 
 /* Distributed context: this rank's part of the box, device data + a peer
  * window.  Connect it with the windows of all ranks (blobs gathered by the
- * application, e.g. torch.distributed.all_gather_object) before any call. */
+ * application, e.g. torch.distributed.all_gather_object) before any call.
+ * Contract of the distributed FAST pcg: the right-hand side must be
+ * continuous across ranks and masked (as every reference caller passes it:
+ * gs_sum then * inv_mult * mask).  Each rank checks its own shared groups and
+ * the pcg returns SBX_E_SHAPE on any rank's violation; copies that differ
+ * ACROSS ranks are not detected (the fused p'Ap identity then gives a wrong
+ * alpha).  An exchange timeout (SBX_E_COMM) leaves the context unusable. */
 sbx_status sbx_ctx_create_box_dist(const sbx_box_desc* desc, const int32_t* rank_of,
                                    int nranks, int rank, int device, sbx_ctx** out);
 /* size of one rank's window blob; this rank's blob */
