@@ -57,13 +57,13 @@ __device__ __forceinline__ void sts2(double* p, double a, double b) {
   *reinterpret_cast<double2*>(p) = make_double2(a, b);
 }
 
-template <int NV, int GROUPS, int SPG>
+template <int NV, int GROUPS, int NSLOT>
 struct DmmaLayout {
   static constexpr int n3 = 512;
   static constexpr int G_D = 24;  // the element's trilinear map coefficients
   static constexpr int V_D = 512;
   static constexpr int SLOT_D = G_D + NV * V_D;
-  static constexpr int S = GROUPS * SPG;
+  static constexpr int S = NSLOT;
   static constexpr size_t BAR_BYTES = 1024;
   static constexpr int AUX_D = 64 + 16;  // D (row-major) and GLL x[8], w[8]
   static constexpr size_t smem = BAR_BYTES + sizeof(double) * (size_t)(AUX_D + S * SLOT_D);
@@ -71,42 +71,36 @@ struct DmmaLayout {
   static_assert(NV >= 3, "the u / sr / ss tiles overlay three staged vectors");
 };
 
-#ifndef SBX_DMMA_SPG
-#define SBX_DMMA_SPG 2  // slots per consumer warp (A/B knob)
-#endif
 #ifndef SBX_DMMA_MAXG
-#define SBX_DMMA_MAXG 6  // consumer warps (A/B knob)
+#define SBX_DMMA_MAXG 7  // consumer warps: 7 + the producer = 256 threads -> 255 registers
 #endif
 #ifndef SBX_CONS_SUSPEND
 #define SBX_CONS_SUSPEND 0  // consumers wait for their slot suspended (A/B knob)
 #endif
 
+// Slots are a shared ring (not owned per warp): as many as fit, each unit m
+// (element) goes to slot m % S and warp m % GROUPS.  A consumer first waits
+// for the slot's unit tag to read m -- the producer writes it only after the
+// slot's previous unit was released -- so its parity wait on the full barrier
+// can never match a phase two back.
 template <int NV>
 struct DmmaChoice {
   static constexpr size_t BUDGET = 225 * 1024;
-  static constexpr int SPG = SBX_DMMA_SPG;
-  // at most 6 consumer warps: each holds ~250 registers (two columns'
-  // metric constants, the t-derivatives and the accumulators)
-  static constexpr int pick() {
-    for (int g = SBX_DMMA_MAXG; g >= 1; --g)
-      if (DmmaLayout<NV, 1, 1>::BAR_BYTES +
-              sizeof(double) * (DmmaLayout<NV, 1, 1>::AUX_D +
-                                (size_t)SPG * g * DmmaLayout<NV, 1, 1>::SLOT_D) <=
-          BUDGET)
-        return g;
-    return 0;
-  }
-  static constexpr int GROUPS = pick();
+  using L1 = DmmaLayout<NV, 1, 1>;
+  static constexpr size_t FIXED = L1::BAR_BYTES + sizeof(double) * L1::AUX_D;
+  static constexpr int fit = (int)((BUDGET - FIXED) / (sizeof(double) * L1::SLOT_D));
+  static constexpr int S = fit > 16 ? 16 : fit;
+  static constexpr int GROUPS = (S - 1) < SBX_DMMA_MAXG ? (S - 1) : SBX_DMMA_MAXG;
   static constexpr bool ok = GROUPS >= 1;
 };
 
 // Pol: the CG K1 policy of cg.cu (CgK1Pol): vec(q), pro(), epi(), hb_of(),
 // finish(), send_index(), element_done(); BMQ = index of bm (or -1).
-template <class Pol, int GROUPS, int SPG>
-__global__ void __launch_bounds__(DmmaLayout<Pol::NV, GROUPS, SPG>::threads, 1)
+template <class Pol, int GROUPS, int NSLOT>
+__global__ void __launch_bounds__(DmmaLayout<Pol::NV, GROUPS, NSLOT>::threads, 1)
     k1_dmma_kernel(typename Pol::Args args, const double* __restrict__ TL, int64_t E, double h1,
                    DParam<8> Dp, double* __restrict__ partials, QParam<8> Qp) {
-  using L = DmmaLayout<Pol::NV, GROUPS, SPG>;
+  using L = DmmaLayout<Pol::NV, GROUPS, NSLOT>;
   constexpr int n = 8;
   constexpr int NV = Pol::NV;
   constexpr int S = L::S;
@@ -119,7 +113,8 @@ __global__ void __launch_bounds__(DmmaLayout<Pol::NV, GROUPS, SPG>::threads, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
   uint64_t* empty = full + S;
   int* meta = reinterpret_cast<int*>(empty + S);
-  static_assert(S * 16 + S * 4 <= L::BAR_BYTES, "barrier area");
+  int* tag = meta + S;  // unit index the slot currently holds (-1: none yet)
+  static_assert(S * 16 + S * 8 <= L::BAR_BYTES, "barrier area");
   double* sD = reinterpret_cast<double*>(smraw + L::BAR_BYTES);  // D[i][l], row-major
   double* sQ = sD + 64;                                           // x[8], w[8]
   double* slots = sD + L::AUX_D;
@@ -129,6 +124,7 @@ __global__ void __launch_bounds__(DmmaLayout<Pol::NV, GROUPS, SPG>::threads, 1)
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
+      tag[s] = -1;
     }
     mbar_fence_init();
   }
@@ -185,6 +181,7 @@ __global__ void __launch_bounds__(DmmaLayout<Pol::NV, GROUPS, SPG>::threads, 1)
           meta[s] = 0;
         }
         double* slot = slots + s * L::SLOT_D;
+        *reinterpret_cast<volatile int*>(&tag[s]) = (int)m;
         mbar_expect_tx(&full[s], 24 * 8 + NV * 512 * 8);
         tma_load_1d(slot, TL + e * 24, 24 * 8, &full[s]);
 #pragma unroll
@@ -206,6 +203,7 @@ __global__ void __launch_bounds__(DmmaLayout<Pol::NV, GROUPS, SPG>::threads, 1)
     for (int64_t m = g; m < M; m += GROUPS) {
       const int s = (int)(m % S);
       const int64_t e = blockIdx.x + m * gridDim.x;
+      while (*reinterpret_cast<volatile int*>(&tag[s]) != (int)m) __nanosleep(20);
       if (SBX_CONS_SUSPEND)
         mbar_wait_backoff(&full[s], (uint32_t)((m / S) & 1));
       else

@@ -1185,8 +1185,8 @@ cudaError_t launch_k1_dmma(const OpDev& op, const double* r, const double* dinv,
   if constexpr (!Ch::ok) {
     return cudaErrorNotSupported;
   } else {
-    using L = DmmaLayout<Pol::NV, Ch::GROUPS, Ch::SPG>;
-    auto kern = k1_dmma_kernel<Pol, Ch::GROUPS, Ch::SPG>;
+    using L = DmmaLayout<Pol::NV, Ch::GROUPS, Ch::S>;
+    auto kern = k1_dmma_kernel<Pol, Ch::GROUPS, Ch::S>;
     static std::atomic<bool> attr_set[64];
     if (!attr_set[dev & 63]) {
       cudaError_t err =
