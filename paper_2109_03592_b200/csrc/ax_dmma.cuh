@@ -57,6 +57,13 @@ __device__ __forceinline__ void sts2(double* p, double a, double b) {
   *reinterpret_cast<double2*>(p) = make_double2(a, b);
 }
 
+#ifndef SBX_DMMA_SELF
+// 1: the consumer warps refill the ring themselves (a warp that releases slot
+// s issues the loads of the unit S ahead into it), so all 8 warps of a
+// 256-thread CTA compute; 0: a dedicated producer warp (A/B knob)
+#define SBX_DMMA_SELF 1
+#endif
+
 template <int NV, int GROUPS, int NSLOT>
 struct DmmaLayout {
   static constexpr int n3 = 512;
@@ -67,12 +74,14 @@ struct DmmaLayout {
   static constexpr size_t BAR_BYTES = 1024;
   static constexpr int AUX_D = 64 + 16;  // D (row-major) and GLL x[8], w[8]
   static constexpr size_t smem = BAR_BYTES + sizeof(double) * (size_t)(AUX_D + S * SLOT_D);
-  static constexpr int threads = GROUPS * 32 + 32;
+  // self-refilling ring (SBX_DMMA_SELF): no producer warp
+  static constexpr int threads = GROUPS * 32 + (SBX_DMMA_SELF ? 0 : 32);
   static_assert(NV >= 3, "the u / sr / ss tiles overlay three staged vectors");
 };
 
 #ifndef SBX_DMMA_MAXG
-#define SBX_DMMA_MAXG 7  // consumer warps: 7 + the producer = 256 threads -> 255 registers
+// consumer warps: 256 threads in all -> up to 255 registers per thread
+#define SBX_DMMA_MAXG (SBX_DMMA_SELF ? 8 : 7)
 #endif
 #ifndef SBX_CONS_SUSPEND
 #define SBX_CONS_SUSPEND 0  // consumers wait for their slot suspended (A/B knob)
@@ -153,7 +162,21 @@ __global__ void __launch_bounds__(DmmaLayout<Pol::NV, GROUPS, NSLOT>::threads, 1
 
   double red = 0.0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp == GROUPS) {
+  // arm slot m % S for unit m and start its loads (one thread)
+  auto issue = [&](int64_t m) {
+    const int s = (int)(m % S);
+    const int64_t e = blockIdx.x + m * gridDim.x;
+    double* slot = slots + s * L::SLOT_D;
+    *reinterpret_cast<volatile int*>(&tag[s]) = (int)m;
+    mbar_expect_tx(&full[s], 24 * 8 + NV * 512 * 8);
+    tma_load_1d(slot, TL + e * 24, 24 * 8, &full[s]);
+#pragma unroll
+    for (int q = 0; q < NV; ++q)
+      tma_load_1d(slot + L::G_D + q * L::V_D, Pol::vec(args_l, q) + e * 512, 512 * 8, &full[s]);
+  };
+  if (SBX_DMMA_SELF && threadIdx.x == 0)
+    for (int64_t m = 0; m < M && m < S; ++m) issue(m);
+  if (!SBX_DMMA_SELF && warp == GROUPS) {
     // ---------------- producer warp: one lane drives the TMA ring ----------
     if (lane == 0) {
       constexpr int PD = 4;
@@ -180,14 +203,8 @@ __global__ void __launch_bounds__(DmmaLayout<Pol::NV, GROUPS, NSLOT>::threads, 1
         } else {
           meta[s] = 0;
         }
-        double* slot = slots + s * L::SLOT_D;
-        *reinterpret_cast<volatile int*>(&tag[s]) = (int)m;
-        mbar_expect_tx(&full[s], 24 * 8 + NV * 512 * 8);
-        tma_load_1d(slot, TL + e * 24, 24 * 8, &full[s]);
-#pragma unroll
-        for (int q = 0; q < NV; ++q)
-          tma_load_1d(slot + L::G_D + q * L::V_D, Pol::vec(args_l, q) + e * 512, 512 * 8,
-                      &full[s]);
+        (void)e;
+        issue(m);
       }
     }
   } else {
@@ -208,7 +225,13 @@ __global__ void __launch_bounds__(DmmaLayout<Pol::NV, GROUPS, NSLOT>::threads, 1
         mbar_wait_backoff(&full[s], (uint32_t)((m / S) & 1));
       else
         mbar_wait(&full[s], (uint32_t)((m / S) & 1));
-      const int nsend = meta[s];
+      int nsend;
+      if constexpr (SBX_DMMA_SELF) {
+        const int32_t* soff = Pol::send_index(args_l);  // multi-GPU send CSR, or null
+        nsend = soff ? __ldg(soff + e + 1) - __ldg(soff + e) : 0;
+      } else {
+        nsend = meta[s];
+      }
       double* slot = slots + s * L::SLOT_D;
       double* V = slot + L::G_D;
       double* tu = V;          // u tile   (overlays r)
@@ -381,7 +404,13 @@ __global__ void __launch_bounds__(DmmaLayout<Pol::NV, GROUPS, NSLOT>::threads, 1
       Pol::element_done(args_l, nsend, e, 1, 512, lane, 32, 1 + g);
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
+      if (lane == 0) {
+        if (SBX_DMMA_SELF) {
+          if (m + S < M) issue(m + S);  // refill the slot just released
+        } else {
+          mbar_arrive(&empty[s]);
+        }
+      }
     }
   }
   Pol::finish(args_l, red, partials, red_sm, &last_flag);
