@@ -103,6 +103,24 @@ def ax_microbench(peak, reps=10):
             "frac": gbs / peak}
 
 
+def bench_config(ex, ey, ez, N, iters, world):
+    """The workload, identical in both arms (the reference arm times a bounded
+    sample of exactly this; its sampling details are in its cpu_baseline)."""
+    nodes = ex * ey * ez * (N + 1) ** 3
+    return {"workload": "Poisson PCG, Jacobi, deformed box (a=0.05), zero guess",
+            "elements": [ex, ey, ez], "degree": N, "local_nodes": nodes,
+            "iterations_per_step": iters, "parallelism": f"rcb{world}",
+            "l2": (f"inputs larger than L2 (per-iteration working set {nodes * 88.4 / 1e9:.1f} "
+                   "GB >> 126 MB)") if nodes * 88.4 > 1e9 else
+                  f"working set {nodes * 88.4 / 1e6:.0f} MB: comparable to L2 (not the bench size)"}
+
+
+def k1_kernel_name(N):
+    if k1_geometry(N) == "trilinear" and N == 7 and not os.environ.get("SBX_K1_FMA"):
+        return "k1_dmma_kernel (K1 on the FP64 tensor cores: p/x update + axhelm + p'Ap)"
+    return "ax_tma_kernel (K1: p/x update + axhelm + p'Ap)"
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -319,13 +337,11 @@ def run_reference_arm(args):
             "ms_per_iteration": s["ms_per_iteration"], "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": "Poisson PCG, Jacobi, deformed box (a=0.05), zero guess",
-                       "elements": [ex, ey, ez], "degree": N,
-                       "iterations_per_step": args.iters,
-                       "parallelism": f"reference CPU pcg, {cores} host threads",
-                       "timed_sample": {"elements": [ex, ey, ez],
-                                        "iterations_per_timed_step": iters},
-                       "setup_s": round(t_setup, 2)},
+            "config": bench_config(ex, ey, ez, N, args.iters, args.gpus),
+            "arm": {"parallelism": f"reference CPU pcg, {cores} host threads",
+                    "timed_sample": {"elements": [ex, ey, ez],
+                                     "iterations_per_timed_step": iters},
+                    "setup_s": round(t_setup, 2)},
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores,
                              "kind": "reference" if backend == "ref" else "port",
                              "cpu_model": cpu_model(), "sample": sample,
@@ -424,18 +440,15 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms, "ms_per_iteration": ms / iters,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": "Poisson PCG, Jacobi, deformed box (a=0.05), zero guess",
-                       "elements": [ex, ey, ez], "degree": N, "local_nodes": nodes,
-                       "iterations_per_step": iters, "parallelism": "rcb1",
-                       "l2": "inputs larger than L2 (per-iteration working set "
-                             f"{nodes * 152 / 1e9:.1f} GB >> 126 MB)",
-                       "setup_s": round(t_setup, 2)},
+            "config": bench_config(ex, ey, ez, N, iters, 1),
+            "arm": {"parallelism": "one B200, FAST solver (one CUDA graph per solve)",
+                    "setup_s": round(t_setup, 2)},
             "e2e": {"value": e2e_val, "unit": UNIT, "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": 2 * 8 * nodes, "d2h_bytes_per_step": 8 * nodes},
-            "gpu_launches": args.steps * (2 * iters + 4),
+            # per solve: rhs check, prologue, 2 per iteration (K1, K2), final update
+            "gpu_launches": args.steps * (2 * iters + 3),
             "roofline": roofline_block(N, ex * ey * ez, nodes, k1_ms, k2_ms, ms / iters, peak,
-                                       peak_kind, traffic,
-                                       "ax_tma_kernel (K1: p/x update + axhelm + p'Ap)"),
+                                       peak_kind, traffic, k1_kernel_name(N)),
             "clocks": clk.summary()}
     line["unique_dof_gdofs"] = value * unique_fraction(ex, ey, ez, N)
     if not args.no_ax_microbench:
@@ -544,14 +557,10 @@ def run_ours_dist(args):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
                 "ms_per_iteration": ms / iters, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": "Poisson PCG, Jacobi, deformed box (a=0.05), zero guess",
-                           "elements": [ex, ey, ez], "degree": N,
-                           "local_nodes_total": nodes_global,
-                           "elements_per_rank": ctx.elem_count,
-                           "iterations_per_step": iters,
-                           "parallelism": f"rcb{world} (elements partitioned, peer-window "
-                                          "halo + scalar exchange over NVLink)",
-                           "l2": "inputs larger than L2", "setup_s": round(t_setup, 2)},
+                "config": bench_config(ex, ey, ez, N, iters, world),
+                "arm": {"parallelism": f"rcb{world}: elements partitioned, peer-window halo "
+                                       "+ scalar exchange over NVLink",
+                        "elements_per_rank": ctx.elem_count, "setup_s": round(t_setup, 2)},
                 "e2e": {"value": nodes_global * iters / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,
                         "ms_per_step": e2e_ms, "h2d_bytes_per_step": 2 * 8 * nodes_global,
                         "d2h_bytes_per_step": 8 * nodes_global},
@@ -559,7 +568,7 @@ def run_ours_dist(args):
                 "roofline": roofline_block(N, ctx.elem_count, ctx.nodes,
                                            ax_ms / max(ax_n, 1), up_ms / max(up_n, 1),
                                            ms / iters, peak, peak_kind, None,
-                                           "ax_tma_kernel (K1, rank 0); k2_ms = halo "
+                                           k1_kernel_name(N) + " on rank 0; k2_ms = halo "
                                            "assembly + K2 + scalar exchange"),
                 "clocks": clocks,
                 "unique_dof_gdofs": value * unique_fraction(ex, ey, ez, N)}

@@ -373,6 +373,10 @@ __global__ void __launch_bounds__(kPThreads)
 // inputs in registers, the 1-D operator as compile-time constant-bank operands
 // (kernel parameters), every component of a pass in flight at once
 // (CP = 3) or one component per pass (CP = 1, less shared memory).
+#ifndef SBX_PENCIL_THREADS
+#define SBX_PENCIL_THREADS 128  // threads per CTA of the pencil kernels (A/B knob)
+#endif
+
 template <int n>
 struct PMatK {
   static constexpr int m = n - 2;
@@ -389,7 +393,7 @@ struct PGrad2 {
 };
 
 template <int n, int CP, bool CG>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(SBX_PENCIL_THREADS)
     p_grad2_kernel(const double* __restrict__ pin, int64_t E, const double* __restrict__ TL,
                    PMatK<n> M, double* __restrict__ g0, double* __restrict__ g1,
                    double* __restrict__ g2, PCgArgs cg) {
@@ -525,7 +529,7 @@ struct PDiv2 {
 };
 
 template <int n, int CP, bool CG>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(SBX_PENCIL_THREADS)
     p_div2_kernel(const double* __restrict__ v0, const double* __restrict__ v1,
                   const double* __restrict__ v2, int64_t E, const double* __restrict__ TL,
                   PMatK<n> M, double* __restrict__ qout, const double* __restrict__ pdot,
@@ -916,12 +920,12 @@ cudaError_t grad_t(const PresDev& P, const double* p, double* const g[3], const 
     if (cg) {
       cudaError_t e = set_smem(p_grad2_kernel<n, CP, true>, sm);
       if (e != cudaSuccess) return e;
-      p_grad2_kernel<n, CP, true><<<pgrid(P.E), 128, sm, s>>>(nullptr, P.E, P.tl, M, g[0], g[1],
+      p_grad2_kernel<n, CP, true><<<pgrid(P.E), SBX_PENCIL_THREADS, sm, s>>>(nullptr, P.E, P.tl, M, g[0], g[1],
                                                               g[2], *cg);
     } else {
       cudaError_t e = set_smem(p_grad2_kernel<n, CP, false>, sm);
       if (e != cudaSuccess) return e;
-      p_grad2_kernel<n, CP, false><<<pgrid(P.E), 128, sm, s>>>(p, P.E, P.tl, M, g[0], g[1],
+      p_grad2_kernel<n, CP, false><<<pgrid(P.E), SBX_PENCIL_THREADS, sm, s>>>(p, P.E, P.tl, M, g[0], g[1],
                                                                g[2], PCgArgs{});
     }
     return cudaGetLastError();
@@ -954,12 +958,12 @@ cudaError_t div_t(const PresDev& P, const double* const v[3], double* q, const d
     if (sc) {
       cudaError_t e = set_smem(p_div2_kernel<n, CP, true>, sm);
       if (e != cudaSuccess) return e;
-      p_div2_kernel<n, CP, true><<<pgrid(P.E), 128, sm, s>>>(v[0], v[1], v[2], P.E, P.tl, M, q,
+      p_div2_kernel<n, CP, true><<<pgrid(P.E), SBX_PENCIL_THREADS, sm, s>>>(v[0], v[1], v[2], P.E, P.tl, M, q,
                                                              pdot, partials, sc);
     } else {
       cudaError_t e = set_smem(p_div2_kernel<n, CP, false>, sm);
       if (e != cudaSuccess) return e;
-      p_div2_kernel<n, CP, false><<<pgrid(P.E), 128, sm, s>>>(v[0], v[1], v[2], P.E, P.tl, M, q,
+      p_div2_kernel<n, CP, false><<<pgrid(P.E), SBX_PENCIL_THREADS, sm, s>>>(v[0], v[1], v[2], P.E, P.tl, M, q,
                                                               nullptr, nullptr, nullptr);
     }
     return cudaGetLastError();

@@ -68,6 +68,22 @@ def main():
     its = [r.iterations for r in rm]
     out["velocity_batched"] = {"ms": ms_m, "iterations": its, "ms_three_single_solves": ms_s,
                                "gdofs": nodes * sum(its) / (ms_m * 1e-3) / 1e9}
+    # --- per-solve overhead: a 20-iteration Poisson solve against 20 iterations
+    # of a 100-iteration one (the difference is the prologue + final update)
+    opp = sb.HelmholtzOperator(ctx, sb.HelmholtzCoeffs(1.0, 0.0))
+    xp = torch.zeros_like(bs[0])
+
+    def solve(k):
+        xp.zero_()
+        return sb.pcg(opp, bs[0], xp, sb.KrylovConfig(0.0, k), history=False)
+
+    ms20, _ = timed(lambda: solve(20))
+    ms100, _ = timed(lambda: solve(100), reps=3)
+    per_it = (ms100 - ms20) / 80
+    out["per_solve_overhead"] = {"ms_20_iterations": ms20, "ms_100_iterations": ms100,
+                                 "ms_per_iteration": per_it,
+                                 "outside_iterations_ms": ms20 - 20 * per_it,
+                                 "fraction_of_20_iteration_solve": (ms20 - 20 * per_it) / ms20}
     # --- pressure
     E = sb.PressureOperator(ctx)
     Np = E.nodes
