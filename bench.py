@@ -99,6 +99,8 @@ def ax_microbench(peak, reps=10):
     gbs = 72 * nodes / (tmin * 1e-3) / 1e9
     return {"config": "Helmholtz Ax h1=h2=1, 32^3 N=7 deformed box, 1 GPU (BASELINE configs[1])",
             "ms_min": tmin, "ms_median": tmed, "gdofs": nodes / (tmin * 1e-3) / 1e9,
+            "kernel": ("ax_tma_kernel (FMA)" if os.environ.get("SBX_K1_FMA") else
+                       "ax_dmma_kernel (FP64 tensor cores, stored G)"),
             "algorithmic_bytes_per_node": 72, "achieved_gbs": gbs, "peak": peak,
             "frac": gbs / peak}
 

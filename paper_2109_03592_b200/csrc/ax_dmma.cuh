@@ -416,4 +416,168 @@ __global__ void __launch_bounds__(DmmaLayout<Pol::NV, GROUPS, NSLOT>::threads, 1
   Pol::finish(args_l, red, partials, red_sm, &last_flag);
 }
 
+// ---- standalone axhelm at n = 8 on the FP64 tensor cores (stored geometry) --
+// The same warp-per-element DMMA scheme for the operator alone (the BASELINE
+// configs[1] microbench): each slot holds the element's packed G [6][512],
+// u [, bm]; per plane the two columns' six factors are read into registers,
+// and after a __syncwarp the plane's sr / ss values overwrite the g1 / g2
+// planes just consumed (the u tile overlays u).  w = h1 D^T G D u + h2 bm u.
+template <bool HAS_BM>
+struct AxDmmaLayout {
+  static constexpr int NV = HAS_BM ? 2 : 1;
+  static constexpr int SLOT_D = 6 * 512 + NV * 512;
+  static constexpr size_t BAR_BYTES = 1024;
+  static constexpr int AUX_D = 64;
+  static constexpr size_t BUDGET = 225 * 1024;
+  static constexpr int fit =
+      (int)((BUDGET - BAR_BYTES - sizeof(double) * AUX_D) / (sizeof(double) * SLOT_D));
+  static constexpr int S = fit > 16 ? 16 : fit;
+  static constexpr int GROUPS = (S - 1) < 8 ? (S - 1) : 8;
+  static constexpr size_t smem = BAR_BYTES + sizeof(double) * (size_t)(AUX_D + S * SLOT_D);
+  static constexpr int threads = GROUPS * 32;
+};
+
+template <bool HAS_BM>
+__global__ void __launch_bounds__(AxDmmaLayout<HAS_BM>::threads, 1)
+    ax_dmma_kernel(const double* __restrict__ U, const double* __restrict__ G,
+                   const double* __restrict__ BM, double* __restrict__ W, int64_t E, double h1,
+                   double h2, double tsign, DParam<8> Dp) {
+  using L = AxDmmaLayout<HAS_BM>;
+  constexpr int n = 8, S = L::S, GROUPS = L::GROUPS, NV = L::NV;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
+  int* tag = reinterpret_cast<int*>(full + S);
+  static_assert(S * 8 + S * 4 <= L::BAR_BYTES, "barrier area");
+  double* sD = reinterpret_cast<double*>(smraw + L::BAR_BYTES);
+  double* slots = sD + L::AUX_D;
+  const int64_t M = E > (int64_t)blockIdx.x ? (E - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      tag[s] = -1;
+    }
+    mbar_fence_init();
+  }
+  if (threadIdx.x < 32) {
+    const int l = threadIdx.x;
+#pragma unroll
+    for (int q = 0; q < 64; q += 32) {
+      double v = 0.0;
+#pragma unroll
+      for (int t = 0; t < 32; ++t)
+        if (l == t) v = Dp.d[q + t];
+      sD[q + l] = v;
+    }
+  }
+  __syncthreads();
+  auto issue = [&](int64_t m) {
+    const int s = (int)(m % S);
+    const int64_t e = blockIdx.x + m * gridDim.x;
+    double* slot = slots + s * L::SLOT_D;
+    *reinterpret_cast<volatile int*>(&tag[s]) = (int)m;
+    mbar_expect_tx(&full[s], (6 + NV) * 512 * 8);
+    tma_load_1d(slot, G + e * 6 * 512, 6 * 512 * 8, &full[s]);
+    tma_load_1d(slot + 6 * 512, U + e * 512, 512 * 8, &full[s]);
+    if (HAS_BM) tma_load_1d(slot + 7 * 512, BM + e * 512, 512 * 8, &full[s]);
+  };
+  if (threadIdx.x == 0)
+    for (int64_t m = 0; m < M && m < S; ++m) issue(m);
+  const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int jr = lane >> 2, q4 = lane & 3, i0 = 2 * q4;
+  const double dA0 = sD[jr * 8 + q4], dA1 = sD[jr * 8 + q4 + 4];
+  const double dB0 = sD[q4 * 8 + jr], dB1 = sD[(q4 + 4) * 8 + jr];
+  for (int64_t m = g; m < M; m += GROUPS) {
+    const int s = (int)(m % S);
+    const int64_t e = blockIdx.x + m * gridDim.x;
+    while (*reinterpret_cast<volatile int*>(&tag[s]) != (int)m) __nanosleep(20);
+    mbar_wait(&full[s], (uint32_t)((m / S) & 1));
+    double* slot = slots + s * L::SLOT_D;
+    double* Gs = slot;               // g1..g6, [6][512]; g1 / g2 planes become sr / ss
+    double* tu = slot + 6 * 512;     // u -> u tile
+    const int64_t ebase = e * 512;
+    double uc0[n], uc1[n];
+#pragma unroll
+    for (int k = 0; k < n; ++k) {
+      const double2 t = lds2(tu + k * 64 + jr * 8 + i0);
+      uc0[k] = t.x;
+      uc1[k] = t.y;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < n; ++k) sts2(tu + k * 64 + dtix(jr, i0), uc0[k], uc1[k]);
+    __syncwarp();
+    double ut0[n], ut1[n];
+#pragma unroll
+    for (int k = 0; k < n; ++k) {
+      double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+      for (int l = 0; l < n; ++l) {
+        t0 = fma(Dp.d[k * n + l], uc0[l], t0);
+        t1 = fma(Dp.d[k * n + l], uc1[l], t1);
+      }
+      ut0[k] = t0;
+      ut1[k] = t1;
+    }
+    double wt0[n], wt1[n];
+#pragma unroll
+    for (int k = 0; k < n; ++k) {
+      const double* up = tu + k * 64;
+      double cr0 = 0.0, cr1 = 0.0, cs0 = 0.0, cs1 = 0.0;
+      dmma884(cr0, cr1, up[dtix(jr, q4)], dA0);
+      dmma884(cr0, cr1, up[dtix(jr, q4 + 4)], dA1);
+      dmma884(cs0, cs1, dA0, up[dtix(q4, jr)]);
+      dmma884(cs0, cs1, dA1, up[dtix(q4 + 4, jr)]);
+      // the plane's six factors of both columns (node (i0 | i0+1, jr, k))
+      const int off = k * 64 + jr * 8 + i0;
+      double2 gg[6];
+#pragma unroll
+      for (int c = 0; c < 6; ++c) gg[c] = lds2(Gs + c * 512 + off);
+      __syncwarp();  // every lane has read plane k of g1 / g2: overwrite it
+      const double sr0 = h1 * fma(gg[0].x, cr0, fma(gg[3].x, cs0, gg[4].x * ut0[k]));
+      const double ss0 = h1 * fma(gg[1].x, cs0, fma(gg[3].x, cr0, gg[5].x * ut0[k]));
+      wt0[k] = h1 * fma(gg[2].x, ut0[k], fma(gg[4].x, cr0, gg[5].x * cs0));
+      const double sr1 = h1 * fma(gg[0].y, cr1, fma(gg[3].y, cs1, gg[4].y * ut1[k]));
+      const double ss1 = h1 * fma(gg[1].y, cs1, fma(gg[3].y, cr1, gg[5].y * ut1[k]));
+      wt1[k] = h1 * fma(gg[2].y, ut1[k], fma(gg[4].y, cr1, gg[5].y * cs1));
+      sts2(Gs + k * 64 + dtix(jr, i0), sr0, sr1);
+      sts2(Gs + 512 + k * 64 + dtix(jr, i0), ss0, ss1);
+    }
+    __syncwarp();
+    double ct0[n], ct1[n];
+#pragma unroll
+    for (int k = 0; k < n; ++k) {
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int l = 0; l < n; ++l) {
+        c0 = fma(tsign * Dp.d[l * n + k], wt0[l], c0);
+        c1 = fma(tsign * Dp.d[l * n + k], wt1[l], c1);
+      }
+      ct0[k] = c0;
+      ct1[k] = c1;
+    }
+#pragma unroll
+    for (int k = 0; k < n; ++k) {
+      const double* rp = Gs + k * 64;
+      const double* sp = Gs + 512 + k * 64;
+      double a0 = 0.0, a1 = 0.0;
+      dmma884(a0, a1, rp[dtix(jr, q4)], dB0);
+      dmma884(a0, a1, rp[dtix(jr, q4 + 4)], dB1);
+      dmma884(a0, a1, dB0, sp[dtix(q4, jr)]);
+      dmma884(a0, a1, dB1, sp[dtix(q4 + 4, jr)]);
+      double w0 = a0 + ct0[k], w1 = a1 + ct1[k];
+      const int off = k * 64 + jr * 8 + i0;
+      if constexpr (HAS_BM) {
+        const double2 u = lds2(tu + k * 64 + dtix(jr, i0));
+        const double2 b = lds2(slot + 7 * 512 + off);
+        w0 = fma(h2 * b.x, u.x, w0);
+        w1 = fma(h2 * b.y, u.y, w1);
+      }
+      stg2(W + ebase + off, w0, w1);
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0 && m + S < M) issue(m + S);
+  }
+}
+
 }  // namespace sbx

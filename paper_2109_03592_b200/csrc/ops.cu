@@ -12,6 +12,7 @@
 
 #include "ax_core.cuh"
 #include "ax_tma.cuh"
+#include "ax_dmma.cuh"
 #include "kernels.cuh"
 #include "sbx_internal.h"
 
@@ -177,6 +178,36 @@ cudaError_t launch_ax_tma(const OpDev& op, const double* u, double* w, double h1
 
 inline bool al16(const void* p) { return p == nullptr || ((uintptr_t)p & 15) == 0; }
 
+// n = 8: the operator on the FP64 tensor cores (ax_dmma.cuh), stored geometry
+template <bool HAS_BM>
+cudaError_t launch_ax_dmma(const OpDev& op, const double* u, double* w, double h1, double h2,
+                           double tsign, cudaStream_t s) {
+  using L = AxDmmaLayout<HAS_BM>;
+  auto kern = ax_dmma_kernel<HAS_BM>;
+  static std::atomic<bool> attr_set[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!attr_set[dev & 63]) {
+    cudaError_t err =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::smem);
+    if (err != cudaSuccess) return err;
+    attr_set[dev & 63] = true;
+  }
+  static std::atomic<int> sms[64];
+  if (!sms[dev & 63]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    sms[dev & 63] = v;
+  }
+  DParam<8> Dp;
+  for (int q = 0; q < 64; ++q) Dp.d[q] = op.Dh[q];
+  const int nsm = sms[dev & 63];
+  int64_t grid = nsm > 0 ? nsm : 148;
+  if (grid > op.E) grid = op.E;
+  kern<<<(unsigned)grid, L::threads, L::smem, s>>>(u, op.G, op.bm, w, op.E, h1, h2, tsign, Dp);
+  return cudaGetLastError();
+}
+
 template <int n, bool EXACT>
 cudaError_t launch_ax_t(const OpDev& op, const double* u, double* w, double h1, double h2,
                         double tsign, cudaStream_t s) {
@@ -184,6 +215,12 @@ cudaError_t launch_ax_t(const OpDev& op, const double* u, double* w, double h1, 
   static const bool no_tma = std::getenv("SBX_NO_TMA") != nullptr;
   if (!EXACT && !no_tma && n % 2 == 0 && al16(u) && al16(w) && al16(op.G) &&
       (h2 == 0.0 || al16(op.bm))) {
+    static const bool fma_ax = std::getenv("SBX_K1_FMA") != nullptr;
+    if constexpr (n == 8) {
+      if (!fma_ax)
+        return h2 != 0.0 ? launch_ax_dmma<true>(op, u, w, h1, h2, tsign, s)
+                         : launch_ax_dmma<false>(op, u, w, h1, h2, tsign, s);
+    }
     const cudaError_t e = h2 != 0.0 ? launch_ax_tma<n, true>(op, u, w, h1, h2, tsign, s)
                                     : launch_ax_tma<n, false>(op, u, w, h1, h2, tsign, s);
     if (e != cudaErrorNotSupported) return e;
