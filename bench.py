@@ -545,7 +545,7 @@ def run_ours_dist(args):
     # skipped under SBX_TRACE so the device trace keeps the graph-mode solve
     ax_ms = up_ms = float("nan")
     ax_n = up_n = 1
-    if not os.environ.get("SBX_TRACE"):
+    if not (os.environ.get("SBX_TRACE") or os.environ.get("SBX_TRACE1")):
         ctx.enable_timing(True)
         x.zero_()
         sb.pcg(op, b, x, cfg, history=False)

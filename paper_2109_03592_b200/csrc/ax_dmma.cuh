@@ -118,7 +118,6 @@ __global__ void __launch_bounds__(DmmaLayout<Pol::NV, GROUPS, NSLOT>::threads, 1
   __shared__ bool last_flag;
   typename Pol::Args args_l = args;
   partials = Pol::partials_of(args, partials);
-  if (!Pol::init(args_l)) return;
   uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
   uint64_t* empty = full + S;
   int* meta = reinterpret_cast<int*>(empty + S);
@@ -159,6 +158,11 @@ __global__ void __launch_bounds__(DmmaLayout<Pol::NV, GROUPS, NSLOT>::threads, 1
     }
   }
   __syncthreads();
+  // (launched programmatically after the update kernel: the set-up above
+  // overlaps its tail; r and the scalars are read only from here on)
+  pdl_wait();
+  pdl_trigger();
+  if (!Pol::init(args_l)) return;
 
   double red = 0.0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

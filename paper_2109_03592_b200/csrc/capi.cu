@@ -1679,6 +1679,9 @@ sbx_status upload_dist(sbx_ctx* c, const DistPlan& P, const sbx_box_desc* d) {
   D.seq = static_cast<unsigned long long*>(p);
   SBX_TRY(dalloc(c, &p, 4 * sizeof(unsigned int)));
   D.counter = static_cast<unsigned int*>(p);
+  SBX_TRY(dalloc(c, &p, 2 * sizeof(unsigned int)));
+  D.gbar = static_cast<unsigned int*>(p);
+  SBX_CUDA(cudaMemsetAsync(D.gbar, 0, 2 * sizeof(unsigned int), c->stream));
   SBX_TRY(dalloc(c, &p, sizeof(int)));
   D.status = static_cast<int*>(p);
   SBX_CUDA(cudaMemsetAsync(D.seq, 0, 4 * sizeof(unsigned long long), c->stream));

@@ -24,6 +24,8 @@
 #include <cstring>
 #include <string>
 #include <type_traits>
+#include <vector>
+#include <cstdio>
 
 #include "ax_core.cuh"
 #include "ax_tma.cuh"
@@ -212,6 +214,7 @@ __device__ void CgK1Pol<HAS_DINV, HAS_BM>::finish(const Args& a, double red, dou
     return;
   }
   if (threadIdx.x == 0) {
+    trace_stamp(nullptr, sc->it, 1);
     sc->counter[0] = 0;
     sc->pq = tot;
     if (!isfinite(tot) || tot <= 0.0) {
@@ -338,6 +341,7 @@ __device__ __forceinline__ void update_tail(double rz, double rr, double alpha, 
     return;
   }
   if (threadIdx.x == 0) {
+    trace_stamp(nullptr, sc->it, 5);
     sc->counter[1] = 0;
     const double rnorm = sqrt(rr_new);
     const int it = sc->it;
@@ -670,14 +674,22 @@ __global__ void __launch_bounds__(K2Layout<n, GROUPS, SPG>::threads, 1)
     hist = multi->hist[c];
     partials += c * multi->part_stride;
   }
+  // (launched programmatically after K1: w, alpha and the flags are read only
+  // after pdl_wait)
+  pdl_wait();
+  pdl_trigger();
   if (sc->done) {
     if (use_cond && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 &&
         !(multi && multi_active(multi)))
       cudaGraphSetConditional(cond, 0);
     return;
   }
-  const double alpha = sc->alpha;
-  if (TABLE && blockIdx.x == 0 && threadIdx.x == 0) trace_stamp(dd, sc->it, 4);
+  double alpha = sc->alpha;
+  if constexpr (TABLE) {
+    // multi-GPU: halo wait, alpha and the interface groups, then a grid barrier
+    if (dd && !k2_dist_prologue(*dd, const_cast<double*>(w), sc, cond, use_cond, alpha)) return;
+  }
+  if (!dd && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) trace_stamp(nullptr, sc->it, 4);
   uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
   uint64_t* empty = full + S;
   int32_t* meta = reinterpret_cast<int32_t*>(smraw + L::BAR_BYTES);  // [GROUPS][2][EPG][32]
@@ -1136,6 +1148,35 @@ constexpr int tri_max_groups(int n) { return n <= 8 ? SBX_TRI_G8 : (n <= 12 ? SB
 thread_local const CgMulti* t_multi = nullptr;
 thread_local int t_ncomp = 1;
 
+// SBX_PDL=1: K1 / K2 of the CG loop are launched with programmatic stream
+// serialisation (each kernel's launch and set-up overlap its predecessor's
+// tail; the kernels call pdl_wait before reading its results).  Measured
+// slower at every size (64^3: 2.18 -> 2.33 ms per iteration; 20^3: 83 -> 86
+// us), so off by default.
+bool pdl_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("SBX_PDL");
+    return e && std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, int threads, size_t smem,
+                       cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3((unsigned)threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_on() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // TRI: the metric is formed at each node from the element's trilinear map
 // (op.tl) instead of streaming the 6 stored factors -- 48 fewer bytes per
 // node on an HBM-bound kernel, for ~50 more FP64 operations per node.
@@ -1169,9 +1210,8 @@ cudaError_t launch_k1_tma(const OpDev& op, const double* r, const double* dinv, 
     const int64_t NG = (op.E + TmaGeom<n>::EPG - 1) / TmaGeom<n>::EPG;
     int64_t grid = num_sms(dev);
     if (grid > NG) grid = NG;
-    kern<<<dim3((unsigned)grid, t_ncomp), L::threads, L::smem, s>>>(
-        a, TRI ? op.tl : op.G, op.E, h1, 1.0, Dp, partials, Qp);
-    return cudaGetLastError();
+    return launch_pdl(kern, dim3((unsigned)grid, t_ncomp), L::threads, L::smem, s, a,
+                      TRI ? op.tl : op.G, op.E, h1, 1.0, Dp, partials, Qp);
   }
 }
 
@@ -1205,9 +1245,8 @@ cudaError_t launch_k1_dmma(const OpDev& op, const double* r, const double* dinv,
     a.multi = t_multi;
     int64_t grid = num_sms(dev);
     if (grid > op.E) grid = op.E;
-    kern<<<dim3((unsigned)grid, t_ncomp), L::threads, L::smem, s>>>(a, op.tl, op.E, h1, Dp,
-                                                                     partials, Qp);
-    return cudaGetLastError();
+    return launch_pdl(kern, dim3((unsigned)grid, t_ncomp), L::threads, L::smem, s, a, op.tl,
+                      op.E, h1, Dp, partials, Qp);
   }
 }
 
@@ -1301,10 +1340,9 @@ cudaError_t launch_k2(const OpDev& op, const double* w, double* r, const double*
     int64_t grid = num_sms(dev);
     if (grid > NG) grid = NG;
     BoxP bx{op.ex, op.ey, op.ez, op.per[0], op.per[1], op.per[2]};
-    kern<<<dim3((unsigned)grid, t_ncomp), L::threads, L::smem, s>>>(
-        w, r, dinv, op.E, bx, op.nbr27, op.dd, sc, partials, hist, hist_cap, cond, use_cond,
-        t_multi);
-    return cudaGetLastError();
+    return launch_pdl(kern, dim3((unsigned)grid, t_ncomp), L::threads, L::smem, s, w, r, dinv,
+                      op.E, bx, op.nbr27, op.dd, sc, partials, hist, hist_cap, cond, use_cond,
+                      (const CgMulti*)t_multi);
   }
   // multi-GPU: only the table-driven TMA kernel knows remote neighbours (-2),
   // local element renumbering and the cross-rank r'z / r'r exchange (and
@@ -1433,9 +1471,7 @@ cudaError_t dist_iteration_tail(const OpDev& op, const DistDev& D, double* w, do
   // last CTA exchanges r'z / r'r and takes the scalar step.
   // one thread per interface group: every group's chain of dependent loads
   // (offsets -> codes -> local / NVLink copies) runs concurrently
-  dist_iface_kernel<<<blocks_for(D.n_if, 128, 16384), 128, 0, s>>>(D, 0, 0, w, 1, sc);
-  cudaError_t err = cudaGetLastError();
-  if (err != cudaSuccess) return err;
+  (void)D;
   return k2(op, w, r, dinv, sc, partials, hist, hist_cap, cond, use_cond, s);
 }
 
@@ -1689,9 +1725,32 @@ int CgEngine::solve_graph(const CgRun& run, sbx_pcg_result* res, bool* general) 
   hprm_->tol = run.tol;
   hprm_->max_it = run.max_it;
   CG_CUDA(cudaMemcpyAsync(prm_, hprm_, sizeof(CgParams), cudaMemcpyHostToDevice, s));
+  // SBX_TRACE1=<path>: per-iteration timeline of single-GPU solves (diagnostics)
+  static const char* trace1 = std::getenv("SBX_TRACE1");
+  unsigned long long* tbuf = nullptr;
+  if (trace1) {
+    CG_CUDA(cudaMalloc(&tbuf, sizeof(unsigned long long) * kTraceIters * 8));
+    CG_CUDA(cudaMemsetAsync(tbuf, 0, sizeof(unsigned long long) * kTraceIters * 8, s));
+    CG_CUDA(cudaMemcpyToSymbolAsync(g_trace1, &tbuf, sizeof(tbuf), 0, cudaMemcpyHostToDevice, s));
+  }
   CG_CUDA(cudaGraphLaunch(sexec_, s));
   CG_CUDA(cudaMemcpyAsync(hsc_, sc_, sizeof(CgScalars), cudaMemcpyDeviceToHost, s));
   CG_CUDA(cudaStreamSynchronize(s));
+  if (trace1) {
+    std::vector<unsigned long long> h((size_t)kTraceIters * 8);
+    unsigned long long* none = nullptr;
+    CG_CUDA(cudaMemcpy(h.data(), tbuf, h.size() * 8, cudaMemcpyDeviceToHost));
+    CG_CUDA(cudaMemcpyToSymbol(g_trace1, &none, sizeof(none)));
+    CG_CUDA(cudaFree(tbuf));
+    if (FILE* f = std::fopen((std::string(trace1) + ".rank0").c_str(), "w")) {
+      for (int it = 0; it < kTraceIters && it < hsc_->it; ++it) {
+        std::fprintf(f, "%d", it);
+        for (int c = 0; c < 8; ++c) std::fprintf(f, " %llu", h[(size_t)it * 8 + c]);
+        std::fprintf(f, "\n");
+      }
+      std::fclose(f);
+    }
+  }
   const int pre = hsc_->pre;
   if (pre & kPreRhsBad) return kCgFallback;  // x untouched: the EXACT path runs
   if (pre & kPreNonzeroX) {

@@ -27,8 +27,8 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
   return v;
 }
 
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -42,18 +42,37 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // thread that stored into PEER memory (halo values over NVLink) takes one
 // system-scope fence (__threadfence_system) after its last such store, before
 // its CTA's ticket -- once per storing thread per kernel, not per store.  ONE
-// thread then releases a flag with st.release.sys, whose cumulativity orders
-// every write it has observed -- including its own stores into peer mailboxes
-// -- before the flag.  Readers acquire the flag with ld.acquire.sys.
+// thread then releases the flags (dist_release: a system fence, whose
+// cumulativity orders every write it has observed -- including its own stores
+// into peer mailboxes -- before the relaxed flag stores).  Readers acquire the
+// flag with ld.acquire.sys.
 __device__ __forceinline__ void dist_fence() { __threadfence(); }
 
 __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
   return *reinterpret_cast<const volatile unsigned long long*>(p);
 }
 
-// SBX_TRACE stamp: slot c of iteration it (one thread calls it)
+// SBX_TRACE stamp: slot c of iteration it (one thread calls it).  Single GPU
+// (SBX_TRACE1): the same slots in g_trace1 (0 K1 start, 1 K1 last CTA, 4 K2
+// start, 5 K2 last CTA).
+__device__ unsigned long long* g_trace1 = nullptr;
 __device__ __forceinline__ void trace_stamp(const DistDev* D, int it, int c) {
-  if (D && D->trace) D->trace[(it % kTraceIters) * 8 + c] = globaltimer();
+  if (D && D->trace)
+    D->trace[(it % kTraceIters) * 8 + c] = globaltimer();
+  else if (!D && g_trace1)
+    g_trace1[(it % kTraceIters) * 8 + c] = globaltimer();
+}
+
+// Release `phase` with sequence v to every other rank: ONE system-scope fence
+// (it orders every write this thread has made or observed -- the mailboxes,
+// and through the CTA tickets the halo stores the other threads fenced --
+// before what follows), then relaxed system-scope flag stores: the PTX
+// release pattern, paid once instead of once per peer (st.release.sys fences
+// before each store, ~1 us apiece over NVLink).
+__device__ __forceinline__ void dist_release(const DistDev& D, int phase, unsigned long long v) {
+  __threadfence_system();
+  for (int q = 0; q < D.nranks; ++q)
+    if (q != D.rank) st_relaxed_sys(D.pflags[q] + phase * kMaxRanks + D.rank, v);
 }
 
 // Wait until every other rank released `phase` with sequence >= expected.
@@ -101,8 +120,7 @@ __global__ void dist_put_kernel(DistDev D, int phase, int slot, const double* __
   for (int q = 0; q < D.nranks; ++q)
     for (int c = 0; c < nscal; ++c)
       D.pmbox[q][mbox_index(phase, (int)par, D.rank, c)] = scal[c];
-  for (int q = 0; q < D.nranks; ++q)
-    if (q != D.rank) st_release_sys(D.pflags[q] + phase * kMaxRanks + D.rank, s + 1);
+  dist_release(D, phase, s + 1);
   D.seq[phase] = s + 1;
 }
 
@@ -116,10 +134,125 @@ __device__ __forceinline__ double mbox_sum(const DistDev& D, int phase, int par,
   return v;
 }
 
+// Interface groups [t0, n_if) step dt: sum every copy in canonical order
+// (local copies from f, remote ones from the receive buffer `par` of `slot`)
+// and write the sum to the local copies (s*0 for masked ones when
+// apply_mask).  Local copies are read through L2 (ld.global.cg): in the fused
+// CG update kernel other SMs read these lines afterwards with cp.async, and no
+// stale L1 line may be left behind.
+// A thread's first interface group, its copy codes loaded ahead (they are
+// static tables: the fused update kernel loads them before the halo wait).
+struct IfacePre {
+  static constexpr int kMax = 8;  // copies of a node: at most 8 elements
+  int lo = 0, cnt = -1;            // cnt < 0: no group; > kMax: not preloaded
+  int32_t code[kMax];
+};
+
+__device__ __forceinline__ IfacePre iface_preload(const DistDev& D, int64_t g) {
+  IfacePre p;
+  if (g < D.n_if) {
+    p.lo = D.if_off[g];
+    p.cnt = D.if_off[g + 1] - p.lo;
+#pragma unroll
+    for (int c = 0; c < IfacePre::kMax; ++c)
+      if (c < p.cnt) p.code[c] = D.if_code[p.lo + c];
+  }
+  return p;
+}
+
+__device__ __forceinline__ void dist_iface_groups(const DistDev& D, int slot, int64_t par,
+                                                  double* f, int apply_mask, int64_t t0,
+                                                  int64_t dt, const IfacePre* pre = nullptr) {
+  const double* rb = D.recvb + (int64_t)(slot * 2 + par) * D.recv_total;
+  const int64_t NL = D.nodes_local;
+  if (pre && pre->cnt >= 0 && pre->cnt <= IfacePre::kMax) {
+    double v[IfacePre::kMax];
+#pragma unroll
+    for (int c = 0; c < IfacePre::kMax; ++c) {
+      if (c < pre->cnt) {
+        const int32_t code = pre->code[c];
+        v[c] = code >= NL ? __ldcv(rb + (code - NL)) : __ldcg(f + (code < 0 ? ~code : code));
+      }
+    }
+    double sum = 0.0;
+#pragma unroll
+    for (int c = 0; c < IfacePre::kMax; ++c)
+      if (c < pre->cnt) sum += v[c];
+#pragma unroll
+    for (int c = 0; c < IfacePre::kMax; ++c) {
+      if (c < pre->cnt) {
+        const int32_t code = pre->code[c];
+        if (code >= NL) continue;
+        if (code >= 0)
+          f[code] = sum;
+        else
+          f[~code] = apply_mask ? __dmul_rn(sum, 0.0) : sum;
+      }
+    }
+    t0 += dt;
+  }
+  for (int64_t g = t0; g < D.n_if; g += dt) {
+    const int lo = D.if_off[g], hi = D.if_off[g + 1];
+    double sum = 0.0;
+    for (int c = lo; c < hi; ++c) {
+      const int32_t code = D.if_code[c];
+      double v;
+      if (code >= NL) {
+        v = __ldcv(rb + (code - NL));
+      } else {
+        v = __ldcg(f + (code < 0 ? ~code : code));
+      }
+      sum += v;
+    }
+    for (int c = lo; c < hi; ++c) {
+      const int32_t code = D.if_code[c];
+      if (code >= NL) continue;
+      if (code >= 0)
+        f[code] = sum;
+      else
+        f[~code] = apply_mask ? __dmul_rn(sum, 0.0) : sum;
+    }
+  }
+}
+
+// Grid-wide barrier of a kernel whose CTAs are all resident (the persistent
+// CG update kernel: grid <= #SMs, one CTA per SM).  gbar[0] counts arrivals,
+// gbar[1] is the generation; bounded like the exchange waits.
+__device__ __forceinline__ bool grid_barrier(unsigned int* gbar) {
+  __shared__ int ok;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int* gen = gbar + 1;
+    const unsigned int g0 = *gen;
+    __threadfence();
+    ok = 1;
+    if (atomicAdd(gbar, 1u) == gridDim.x - 1) {
+      gbar[0] = 0;
+      __threadfence();
+      atomicAdd(gbar + 1, 1u);
+    } else {
+      const unsigned long long t0 = globaltimer();
+      unsigned int v;
+      for (int spin = 0;; ++spin) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(gbar + 1) : "memory");
+        if (v != g0) break;
+        if ((spin & 255) == 255 && globaltimer() - t0 > kSpinTimeoutNs) {
+          ok = 0;
+          break;
+        }
+      }
+      __threadfence();
+    }
+  }
+  __syncthreads();
+  return ok != 0;
+}
+
 // Interface groups: wait for the halo, sum every copy in canonical order
 // (local copies from f, remote ones from the receive buffer) and write the sum
 // to the local copies (s*0 for masked ones when apply_mask).  In the CG loop
 // (sc != null) block 0 also forms alpha = rz / sum_q pq_q and tests breakdown.
+// (The fused CG loop does this inside the update kernel: k2_dist_prologue.)
 __global__ void dist_iface_kernel(DistDev D, int phase, int slot, double* __restrict__ f,
                                   int apply_mask, CgScalars* __restrict__ sc) {
   __shared__ bool ok;
@@ -149,33 +282,73 @@ __global__ void dist_iface_kernel(DistDev D, int phase, int slot, double* __rest
       sc->alpha = sc->rz / pq;
     }
   }
-  const int64_t par = (int64_t)(ld_volatile_u64(D.seq + phase) & 1);
   // remote copies were pushed into this rank's receive buffer
-  const double* rb = D.recvb + (int64_t)(slot * 2 + par) * D.recv_total;
-  const int64_t NL = D.nodes_local;
-  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < D.n_if;
-       g += (int64_t)gridDim.x * blockDim.x) {
-    const int lo = D.if_off[g], hi = D.if_off[g + 1];
-    double sum = 0.0;
-    for (int c = lo; c < hi; ++c) {
-      const int32_t code = D.if_code[c];
-      double v;
-      if (code >= NL) {
-        v = __ldcv(rb + (code - NL));
-      } else {
-        v = f[code < 0 ? ~code : code];
-      }
-      sum += v;
-    }
-    for (int c = lo; c < hi; ++c) {
-      const int32_t code = D.if_code[c];
-      if (code >= NL) continue;
-      if (code >= 0)
-        f[code] = sum;
+  dist_iface_groups(D, slot, (int64_t)(ld_volatile_u64(D.seq + phase) & 1), f, apply_mask,
+                    (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                    (int64_t)gridDim.x * blockDim.x);
+}
+
+// Start of the fused multi-GPU CG update kernel (replaces dist_iface_kernel
+// in the loop): every CTA waits for the halo and the p'Ap partials of phase 0,
+// forms alpha = rz / sum_q pq_q itself (rank order: identical bits in every
+// CTA and on every rank), assembles its share of the interface groups into w,
+// and passes a grid barrier before any CTA reads w.  Returns false when the
+// iteration must stop (exchange timeout, breakdown); block 0 records why.
+__device__ bool k2_dist_prologue(const DistDev& D, double* w, CgScalars* __restrict__ sc,
+                                 cudaGraphConditionalHandle cond, int use_cond,
+                                 double& alpha) {
+  __shared__ int st_sm;
+  __shared__ double al_sm;
+  const int it = sc->it;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // this thread's first interface group: codes loaded while thread 0 waits
+  const IfacePre pre = iface_preload(D, t0);
+  if (threadIdx.x == 0) {
+    if (blockIdx.x == 0) trace_stamp(&D, it, 2);
+    const unsigned long long s = ld_volatile_u64(D.seq);
+    int st = dist_wait_all(D, 0, s) ? 0 : 8;
+    double a = 0.0, pq = 0.0;
+    if (!st) {
+      pq = mbox_sum(D, 0, (int)(s & 1), 0);
+      if (!isfinite(pq) || pq <= 0.0)
+        st = 5;
       else
-        f[~code] = apply_mask ? __dmul_rn(sum, 0.0) : sum;
+        a = sc->rz / pq;
     }
+    if (blockIdx.x == 0) {
+      trace_stamp(&D, it, 3);
+      if (st) {
+        if (st == 8) *D.status = 1;
+        sc->status = st;
+        if (st == 5) sc->err_it = it;
+        sc->done = 1;
+        if (use_cond) cudaGraphSetConditional(cond, 0);
+      } else {
+        sc->pq = pq;
+        sc->alpha = a;
+      }
+    }
+    st_sm = st;
+    al_sm = a;
   }
+  __syncthreads();
+  if (st_sm) return false;
+  alpha = al_sm;
+  dist_iface_groups(D, 0, (int64_t)(ld_volatile_u64(D.seq) & 1), w, 1, t0,
+                    (int64_t)gridDim.x * blockDim.x, &pre);
+  if (!grid_barrier(D.gbar)) {
+    if (threadIdx.x == 0) {
+      *D.status = 1;
+      sc->status = 8;
+      sc->done = 1;
+      if (use_cond) cudaGraphSetConditional(cond, 0);
+    }
+    return false;
+  }
+  // the assembled values are read next by TMA (async proxy) and cp.async
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  if (blockIdx.x == 0 && threadIdx.x == 0) trace_stamp(&D, it, 4);
+  return true;
 }
 
 // Scalar all-reduce (rank order) of `count` doubles; one thread.
@@ -186,8 +359,7 @@ __global__ void dist_allreduce_kernel(DistDev D, int phase, const double* __rest
   for (int q = 0; q < D.nranks; ++q)
     for (int c = 0; c < count; ++c)
       D.pmbox[q][mbox_index(phase, (int)((s + 1) & 1), D.rank, c)] = in[c];
-  for (int q = 0; q < D.nranks; ++q)
-    if (q != D.rank) st_release_sys(D.pflags[q] + phase * kMaxRanks + D.rank, s + 1);
+  dist_release(D, phase, s + 1);
   D.seq[phase] = s + 1;
   if (!dist_wait_all(D, phase, s + 1)) {
     *D.status = 1;
@@ -211,8 +383,7 @@ __device__ void dist_scalar_step(const DistDev& D, CgScalars* __restrict__ sc, d
   for (int q = 0; q < D.nranks; ++q)
     for (int c = 0; c < 2; ++c)
       D.pmbox[q][mbox_index(phase, (int)((s + 1) & 1), D.rank, c)] = mine[c];
-  for (int q = 0; q < D.nranks; ++q)
-    if (q != D.rank) st_release_sys(D.pflags[q] + phase * kMaxRanks + D.rank, s + 1);
+  dist_release(D, phase, s + 1);
   D.seq[phase] = s + 1;
   if (!dist_wait_all(D, phase, s + 1)) {
     *D.status = 1;
@@ -281,8 +452,7 @@ __device__ void dist_release_phase0(const DistDev& D, double pq_loc) {
   const unsigned long long s = ld_volatile_u64(D.seq);
   const int par = (int)((s + 1) & 1);
   for (int q = 0; q < D.nranks; ++q) D.pmbox[q][mbox_index(0, par, D.rank, 0)] = pq_loc;
-  for (int q = 0; q < D.nranks; ++q)
-    if (q != D.rank) st_release_sys(D.pflags[q] + D.rank, s + 1);
+  dist_release(D, 0, s + 1);
   D.seq[0] = s + 1;
 }
 

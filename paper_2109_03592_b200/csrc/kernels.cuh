@@ -159,6 +159,7 @@ struct DistDev {
   const int32_t* esend_pos = nullptr;
   unsigned long long* seq = nullptr;  // device [4]
   unsigned int* counter = nullptr;    // device [4]
+  unsigned int* gbar = nullptr;       // device [2]: grid barrier of the update kernel
   int* status = nullptr;              // device: 1 on exchange timeout
   // SBX_TRACE: per-iteration %globaltimer stamps [kTraceIters][8] (diagnostics)
   unsigned long long* trace = nullptr;

@@ -97,6 +97,17 @@ __device__ __forceinline__ void cp_async_wait() {
 
 // Order this thread's generic-proxy shared-memory accesses before later
 // async-proxy (TMA) writes to the same locations.
+// Programmatic dependent launch: a kernel launched with the programmatic
+// stream-serialisation attribute may start while its predecessor still runs;
+// pdl_wait() blocks until the predecessor has completed and its memory is
+// visible (a no-op for a normally launched kernel), pdl_trigger() lets the
+// successor's launch begin.  Every kernel the CG loop launches this way calls
+// pdl_wait() before its first read of anything its predecessors wrote.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
