@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(DmmaLayout<Pol::NV, GROUPS, NSLOT>::threads, 1
   // overlaps its tail; r and the scalars are read only from here on)
   pdl_wait();
   pdl_trigger();
-  if (!Pol::init(args_l)) return;
+  if (!Pol::init_ptrs(args_l)) return;
 
   double red = 0.0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -178,8 +178,17 @@ __global__ void __launch_bounds__(DmmaLayout<Pol::NV, GROUPS, NSLOT>::threads, 1
     for (int q = 0; q < NV; ++q)
       tma_load_1d(slot + L::G_D + q * L::V_D, Pol::vec(args_l, q) + e * 512, 512 * 8, &full[s]);
   };
-  if (SBX_DMMA_SELF && threadIdx.x == 0)
+  // the first loads (thread 32: thread 0 takes the multi-GPU exchange below)
+  constexpr int kIssuer = L::threads > 32 ? 32 : 0;
+  if (SBX_DMMA_SELF && threadIdx.x == kIssuer)
     for (int64_t m = 0; m < M && m < S; ++m) issue(m);
+  // the scalars (multi-GPU: after the r'z / r'r exchange, which the loads
+  // just started overlap); a solve found finished drains the loads first
+  if (!Pol::init_scalars(args_l)) {
+    if (SBX_DMMA_SELF && threadIdx.x == kIssuer)
+      for (int64_t m = 0; m < M && m < S; ++m) mbar_wait(&full[m], 0u);
+    return;
+  }
   if (!SBX_DMMA_SELF && warp == GROUPS) {
     // ---------------- producer warp: one lane drives the TMA ring ----------
     if (lane == 0) {

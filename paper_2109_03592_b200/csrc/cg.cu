@@ -111,7 +111,13 @@ struct CgK1Pol {
   __device__ static double* partials_of(const Args& a, double* partials) {
     return a.multi ? partials + blockIdx.y * a.multi->part_stride : partials;
   }
-  __device__ static bool init(Args& a) {
+  // set-up in two parts (k1_dmma_kernel starts its first loads in between):
+  // init_ptrs: the component's vectors, false when the solve is done;
+  // init_scalars: the scalars of this iteration (multi-GPU: after the
+  // previous iteration's r'z / r'r exchange), false when the exchange found
+  // the solve finished
+  __device__ static bool init(Args& a) { return init_ptrs(a) && init_scalars(a); }
+  __device__ static bool init_ptrs(Args& a) {
     if (a.multi) {
       const int c = blockIdx.y;
       a.r = a.multi->r[c];
@@ -121,13 +127,27 @@ struct CgK1Pol {
       a.sc = a.multi->sc[c];
       a.multi = nullptr;  // (dead from here on: no register held across the sweeps)
     }
-    if (a.sc->done) return false;
+    return !a.sc->done;
+  }
+  __device__ static bool init_scalars(Args& a) {
     a.first = a.sc->first;
     a.beta = a.sc->beta;
     a.ap = a.sc->alpha_prev;
+    if (a.dd) {
+      if (blockIdx.x == 0 && threadIdx.x == 0)
+        trace_stamp(a.dd, a.sc->it + (a.sc->xpend ? 1 : 0), 0);
+      // the previous iteration's r'z / r'r exchange and scalar step
+      const int h = k1_dist_head(*a.dd, a.sc);
+      if (h == 2) return false;
+      if (h == 1) {
+        const DistStep& st = dist_step_smem();
+        a.first = 0;
+        a.beta = st.beta;
+        a.ap = st.alpha_prev;
+      }
+    }
     a.par = a.dd ? (int)((*(const volatile unsigned long long*)a.dd->seq + 1) & 1) : 0;
     a.esend_off = a.dd ? a.dd->esend_off : nullptr;
-    if (blockIdx.x == 0 && threadIdx.x == 0) trace_stamp(a.dd, a.sc->it, 0);
     return true;
   }
   // per-element send offsets (CSR): the producer lane prefetches
@@ -195,10 +215,9 @@ struct CgK1Pol {
 template <bool HAS_DINV, bool HAS_BM>
 __device__ void CgK1Pol<HAS_DINV, HAS_BM>::finish(const Args& a, double red, double* partials,
                                                   double* sh, bool* flag) {
-  // (dist: a thread that pushed halo values over NVLink fences them at
-  // system scope once, here, before the CTA's ticket; the last CTA then
-  // releases them with dist_release_phase0)
-  if (a.stored) __threadfence_system();
+  // (dist: the halo values this kernel pushed over NVLink are released by
+  // the update kernel once this one has completed -- kernel completion makes
+  // them visible system-wide, so no thread fences them here)
   const double v = cta_sum(red, sh);
   if (threadIdx.x == 0) partials[blockIdx.x] = v;
   CgScalars* sc = a.sc;
@@ -206,11 +225,11 @@ __device__ void CgK1Pol<HAS_DINV, HAS_BM>::finish(const Args& a, double red, dou
   const double tot = reduce_partials(partials, gridDim.x, 1, 0, sh);
   if (threadIdx.x == 0 && a.dd) {
     sc->counter[0] = 0;
-    sc->pq_loc = tot;  // summed over ranks by dist_iface_kernel
+    // every CTA has read the scalars: record the step taken at the head
+    if (dist_step_smem().pending) dist_step_commit(sc, dist_step_smem());
+    sc->pq_loc = tot;  // published and summed over ranks by k2_dist_prologue
     trace_stamp(a.dd, sc->it, 1);
-    // every CTA fenced its interface stores before its ticket: release the
-    // halo and this rank's p'Ap to all ranks
-    dist_release_phase0(*a.dd, tot);
+    a.dd->seq[0] += 1;  // phase 0 of this iteration: released by the update kernel
     return;
   }
   if (threadIdx.x == 0) {
@@ -332,12 +351,17 @@ __device__ __forceinline__ void update_tail(double rz, double rr, double alpha, 
   const double rz_new = reduce_partials(partials, gridDim.x, 2, 0, red);
   const double rr_new = reduce_partials(partials, gridDim.x, 2, 1, red);
   if (threadIdx.x == 0 && dd) {
-    // distributed: exchange the rank partials and take the scalar step here
-    // (rank-order sums, so every rank gets identical beta / convergence)
+    // distributed: the rank partials are exchanged and the scalar step taken
+    // at the start of the next K1 (k1_dist_head: rank-order sums, so every
+    // rank gets identical beta / convergence); the kernel boundary publishes
+    // the partials.  The graph condition stays set until a K1 finds the solve
+    // finished and the update kernel after it clears it.
+    trace_stamp(dd, sc->it, 5);
     sc->counter[1] = 0;
     sc->rz_loc = rz_new;
     sc->rr_loc = rr_new;
-    dist_scalar_step(*dd, sc, rz_new, rr_new, hist, hist_cap, cond, use_cond);
+    dd->seq[1] += 1;
+    sc->xpend = 1;
     return;
   }
   if (threadIdx.x == 0) {
@@ -685,11 +709,6 @@ __global__ void __launch_bounds__(K2Layout<n, GROUPS, SPG>::threads, 1)
     return;
   }
   double alpha = sc->alpha;
-  if constexpr (TABLE) {
-    // multi-GPU: halo wait, alpha and the interface groups, then a grid barrier
-    if (dd && !k2_dist_prologue(*dd, const_cast<double*>(w), sc, cond, use_cond, alpha)) return;
-  }
-  if (!dd && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) trace_stamp(nullptr, sc->it, 4);
   uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
   uint64_t* empty = full + S;
   int32_t* meta = reinterpret_cast<int32_t*>(smraw + L::BAR_BYTES);  // [GROUPS][2][EPG][32]
@@ -707,21 +726,49 @@ __global__ void __launch_bounds__(K2Layout<n, GROUPS, SPG>::threads, 1)
   __syncthreads();
   double rz = 0.0, rr = 0.0;
   const int warp = threadIdx.x >> 5;
+  const bool producer = warp == GROUPS * T::TG / 32 && (threadIdx.x & 31) == 0;
+  // the loads of step m: part 1 = r, 1/diag (arms the barrier), part 2 = w
+  auto issue = [&](int64_t m, bool p1, bool p2) {
+    const int s = (int)(m % S);
+    const int64_t e0 = (blockIdx.x + m * gridDim.x) * EPG;
+    const int64_t cnt = (E - e0) < EPG ? (E - e0) : EPG;
+    const int shift = (int)((e0 * T::n3) & 1);
+    const uint32_t vb = (uint32_t)((((cnt * T::n3 + shift) * 8) + 15) / 16 * 16);
+    double* slot = slots + s * L::SLOT_D;
+    if (p1) {
+      mbar_expect_tx(&full[s], (dinv ? 3 : 2) * vb);
+      tma_load_1d(slot + L::V_D, r + e0 * T::n3 - shift, vb, &full[s]);
+      if (dinv) tma_load_1d(slot + 2 * L::V_D, dinv + e0 * T::n3 - shift, vb, &full[s]);
+    }
+    if (p2) tma_load_1d(slot, w + e0 * T::n3 - shift, vb, &full[s]);
+  };
+  int64_t npre = 0;
+  if constexpr (TABLE) {
+    if (dd) {
+      // multi-GPU: r and 1/diag of the first steps stream in while the halo
+      // arrives; then the halo wait, alpha and the interface groups, a grid
+      // barrier, and only then the loads of w
+      if (producer) {
+        npre = M < S ? M : S;
+        for (int64_t m = 0; m < npre; ++m) issue(m, true, false);
+      }
+      if (!k2_dist_prologue(*dd, const_cast<double*>(w), sc, cond, use_cond, alpha)) {
+        if (producer) {  // complete and drain the loads in flight before leaving
+          for (int64_t m = 0; m < npre; ++m) issue(m, false, true);
+          for (int64_t m = 0; m < npre; ++m) mbar_wait(&full[m], 0u);
+        }
+        return;
+      }
+    }
+  }
+  if (!dd && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) trace_stamp(nullptr, sc->it, 4);
   if (warp == GROUPS * T::TG / 32) {
     // ---------------- producer warp: one lane drives the TMA ring --------
-    if ((threadIdx.x & 31) == 0) {
+    if (producer) {
       for (int64_t m = 0; m < M; ++m) {
         const int s = (int)(m % S);
         if (m >= S) mbar_wait_backoff(&empty[s], (uint32_t)((m / S - 1) & 1));
-        const int64_t e0 = (blockIdx.x + m * gridDim.x) * EPG;
-        const int64_t cnt = (E - e0) < EPG ? (E - e0) : EPG;
-        const int shift = (int)((e0 * T::n3) & 1);
-        const uint32_t vb = (uint32_t)((((cnt * T::n3 + shift) * 8) + 15) / 16 * 16);
-        double* slot = slots + s * L::SLOT_D;
-        mbar_expect_tx(&full[s], (dinv ? 3 : 2) * vb);
-        tma_load_1d(slot, w + e0 * T::n3 - shift, vb, &full[s]);
-        tma_load_1d(slot + L::V_D, r + e0 * T::n3 - shift, vb, &full[s]);
-        if (dinv) tma_load_1d(slot + 2 * L::V_D, dinv + e0 * T::n3 - shift, vb, &full[s]);
+        issue(m, m >= npre, true);
       }
     }
   } else {
@@ -1058,6 +1105,8 @@ __global__ void cg_prologue_kernel(int64_t N, const double* __restrict__ b,
   sc->status = 0;
   sc->err_it = -1;
   sc->nranks = 1;
+  sc->xpend = 0;
+  sc->k1_idle = 0;
   sc->converged = 0;
   sc->alpha = sc->alpha_prev = sc->beta = sc->pq = 0.0;
   if (pre) {
@@ -1996,6 +2045,7 @@ int CgEngine::run_timed_loop(const CgRun& run) {
     float a = 0, b = 0;
     cudaEventElapsedTime(&a, ev[0], ev[1]);
     cudaEventElapsedTime(&b, ev[1], ev[2]);
+    if (hsc_->done && hsc_->k1_idle) break;  // (distributed: a K1 that only took the last step)
     t_ax_ms_ += a;
     t_upd_ms_ += b;
     ++n_ax_;
@@ -2109,6 +2159,8 @@ int CgEngine::solve(const CgRun& run, sbx_pcg_result* res) {
   h.done = 0;
   h.err_it = -1;
   h.nranks = D ? D->nranks : 1;
+  h.hist = hist_;
+  h.hist_cap = hist_len_;
   const bool conv0 = rel0 <= run.tol && relp0 <= run.tol;
   if (conv0) {
     h.converged = 1;

@@ -303,13 +303,25 @@ __device__ bool k2_dist_prologue(const DistDev& D, double* w, CgScalars* __restr
   const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   // this thread's first interface group: codes loaded while thread 0 waits
   const IfacePre pre = iface_preload(D, t0);
+  // phase 0 of this iteration (K1 advanced the sequence at its end)
+  const unsigned long long s = ld_volatile_u64(D.seq);
   if (threadIdx.x == 0) {
-    if (blockIdx.x == 0) trace_stamp(&D, it, 2);
-    const unsigned long long s = ld_volatile_u64(D.seq);
+    const double pq_loc = sc->pq_loc;
+    if (blockIdx.x == 0) {
+      trace_stamp(&D, it, 2);
+      // K1 has completed, so the halo it pushed is visible system-wide:
+      // publish this rank's p'Ap and release phase 0 to every peer
+      for (int q = 0; q < D.nranks; ++q)
+        if (q != D.rank) D.pmbox[q][mbox_index(0, (int)(s & 1), D.rank, 0)] = pq_loc;
+      dist_release(D, 0, s);
+    }
     int st = dist_wait_all(D, 0, s) ? 0 : 8;
     double a = 0.0, pq = 0.0;
     if (!st) {
-      pq = mbox_sum(D, 0, (int)(s & 1), 0);
+      // rank order; this rank's own term from sc (identical in every CTA)
+      for (int q = 0; q < D.nranks; ++q)
+        pq += q == D.rank ? pq_loc
+                          : *(const volatile double*)(D.mbox + mbox_index(0, (int)(s & 1), q, 0));
       if (!isfinite(pq) || pq <= 0.0)
         st = 5;
       else
@@ -334,8 +346,7 @@ __device__ bool k2_dist_prologue(const DistDev& D, double* w, CgScalars* __restr
   __syncthreads();
   if (st_sm) return false;
   alpha = al_sm;
-  dist_iface_groups(D, 0, (int64_t)(ld_volatile_u64(D.seq) & 1), w, 1, t0,
-                    (int64_t)gridDim.x * blockDim.x, &pre);
+  dist_iface_groups(D, 0, (int64_t)(s & 1), w, 1, t0, (int64_t)gridDim.x * blockDim.x, &pre);
   if (!grid_barrier(D.gbar)) {
     if (threadIdx.x == 0) {
       *D.status = 1;
@@ -369,57 +380,115 @@ __global__ void dist_allreduce_kernel(DistDev D, int phase, const double* __rest
   for (int c = 0; c < count; ++c) out[c] = mbox_sum(D, phase, (int)((s + 1) & 1), c);
 }
 
-// End of a distributed CG iteration, run by ONE thread (the last CTA of the
-// update kernel): all-reduce r'z, r'r (phase 1) through the mailboxes, then
-// the scalar logic of update_tail (beta, history, convergence, NaN) and the
-// WHILE condition.
-__device__ void dist_scalar_step(const DistDev& D, CgScalars* __restrict__ sc, double rz_loc,
-                                 double rr_loc, double* __restrict__ hist, int64_t hist_cap,
-                                 cudaGraphConditionalHandle cond, int use_cond) {
-  const int phase = 1;
-  const unsigned long long s = ld_volatile_u64(D.seq + phase);
-  const double mine[2] = {rz_loc, rr_loc};
-  trace_stamp(&D, sc->it, 5);
-  for (int q = 0; q < D.nranks; ++q)
-    for (int c = 0; c < 2; ++c)
-      D.pmbox[q][mbox_index(phase, (int)((s + 1) & 1), D.rank, c)] = mine[c];
-  dist_release(D, phase, s + 1);
-  D.seq[phase] = s + 1;
-  if (!dist_wait_all(D, phase, s + 1)) {
-    *D.status = 1;
-    sc->status = 8;
-    sc->done = 1;
-    if (use_cond) cudaGraphSetConditional(cond, 0);
-    return;
-  }
-  trace_stamp(&D, sc->it, 6);
-  const double rz_new = mbox_sum(D, phase, (int)((s + 1) & 1), 0);
-  const double rr_new = mbox_sum(D, phase, (int)((s + 1) & 1), 1);
-  const double rnorm = sqrt(rr_new);
-  const int it = sc->it;
-  if (!isfinite(rnorm) || !isfinite(rz_new)) {
-    sc->status = 6;
-    sc->err_it = it;
+// The distributed scalar step of one iteration (krylov.cpp:51-57, 70-84 with
+// rank-order sums): computed at the start of the next K1 by thread 0 of EVERY
+// CTA from the same mailboxes, so every CTA (and every rank) holds identical
+// values; written to the scalars by the last CTA of that K1 (or, when the
+// solve ends there, by block 0).
+struct DistStep {
+  double beta, rz, rr, rel, relp, alpha_prev;
+  int it_before, it, done, converged, status, pending;
+};
+__device__ __forceinline__ DistStep& dist_step_smem() {
+  __shared__ DistStep st;
+  return st;
+}
+
+__device__ __forceinline__ void dist_step_commit(CgScalars* __restrict__ sc, const DistStep& o) {
+  if (o.status) {
+    sc->status = o.status;
+    if (o.status == 6) sc->err_it = o.it_before;
     sc->done = 1;
   } else {
-    const double rel = rnorm / sc->bnorm;
-    if (hist && it + 1 < hist_cap) hist[it + 1] = rel;
-    sc->it = it + 1;
-    sc->beta = rz_new / sc->rz;
-    sc->rz = rz_new;
-    sc->rr = rr_new;
-    sc->alpha_prev = sc->alpha;
+    if (sc->hist && o.it_before + 1 < sc->hist_cap) sc->hist[o.it_before + 1] = o.rel;
+    sc->it = o.it;
+    sc->beta = o.beta;
+    sc->rz = o.rz;
+    sc->rr = o.rr;
+    sc->alpha_prev = o.alpha_prev;
     sc->first = 0;
-    sc->rel = rel;
-    sc->relp = sc->bmb > 0.0 ? sqrt(fmax(rz_new, 0.0) / sc->bmb) : 0.0;
-    if (sc->rel <= sc->tol && sc->relp <= sc->tol) {
-      sc->converged = 1;
-      sc->done = 1;
-    } else if (sc->it >= sc->max_it) {
-      sc->done = 1;
-    }
+    sc->rel = o.rel;
+    sc->relp = o.relp;
+    if (o.converged) sc->converged = 1;
+    if (o.done) sc->done = 1;
   }
-  if (use_cond) cudaGraphSetConditional(cond, sc->done ? 0 : 1);
+  sc->xpend = 0;
+}
+
+// Start of a distributed K1 (all threads call it): when the update kernel
+// left r'z / r'r partials (sc->xpend), publish this rank's (block 0: phase-1
+// mailboxes + release), wait for every peer's, sum in rank order and take the
+// scalar step.  Returns 0: no step pending (first iteration), 1: stepped,
+// iterate; 2: the solve is finished (recorded by block 0; the update kernel
+// that follows sees done and ends the graph loop).
+__device__ int k1_dist_head(const DistDev& D, CgScalars* __restrict__ sc) {
+  __shared__ int res;
+  DistStep& st = dist_step_smem();
+  if (threadIdx.x == 0) {
+    int r = 0;
+    st.pending = 0;
+    if (sc->xpend) {
+      DistStep o{};
+      o.it_before = o.it = sc->it;
+      const unsigned long long s = ld_volatile_u64(D.seq + 1);
+      const int par = (int)(s & 1);
+      const double rz_loc = sc->rz_loc, rr_loc = sc->rr_loc;
+      const bool lead = blockIdx.x == 0 && blockIdx.y == 0;
+      if (lead) {
+        for (int q = 0; q < D.nranks; ++q) {
+          if (q == D.rank) continue;
+          D.pmbox[q][mbox_index(1, par, D.rank, 0)] = rz_loc;
+          D.pmbox[q][mbox_index(1, par, D.rank, 1)] = rr_loc;
+        }
+        dist_release(D, 1, s);
+      }
+      if (!dist_wait_all(D, 1, s)) {
+        o.status = 8;
+        o.done = 1;
+        if (lead) *D.status = 1;
+      } else {
+        if (lead) trace_stamp(&D, o.it_before + 1, 6);
+        double rz_new = 0.0, rr_new = 0.0;
+        for (int q = 0; q < D.nranks; ++q) {
+          const volatile double* m = D.mbox + mbox_index(1, par, q, 0);
+          rz_new += q == D.rank ? rz_loc : m[0];
+        }
+        for (int q = 0; q < D.nranks; ++q) {
+          const volatile double* m = D.mbox + mbox_index(1, par, q, 1);
+          rr_new += q == D.rank ? rr_loc : m[0];
+        }
+        const double rnorm = sqrt(rr_new);
+        if (!isfinite(rnorm) || !isfinite(rz_new)) {
+          o.status = 6;
+          o.done = 1;
+        } else {
+          o.rel = rnorm / sc->bnorm;
+          o.it = o.it_before + 1;
+          o.beta = rz_new / sc->rz;
+          o.rz = rz_new;
+          o.rr = rr_new;
+          o.alpha_prev = sc->alpha;
+          o.relp = sc->bmb > 0.0 ? sqrt(fmax(rz_new, 0.0) / sc->bmb) : 0.0;
+          if (o.rel <= sc->tol && o.relp <= sc->tol) {
+            o.converged = 1;
+            o.done = 1;
+          } else if (o.it >= sc->max_it) {
+            o.done = 1;
+          }
+        }
+      }
+      o.pending = 1;
+      st = o;
+      r = o.done ? 2 : 1;
+      if (r == 2 && lead) {
+        dist_step_commit(sc, o);
+        sc->k1_idle = 1;
+      }
+    }
+    res = r;
+  }
+  __syncthreads();
+  return res;
 }
 
 // Sends of one element-step from the Ax epilogue: the group's threads store
@@ -446,15 +515,6 @@ __device__ __forceinline__ bool dist_send_elements(const DistDev* __restrict__ D
   return stored;
 }
 
-// Release of phase 0 by the last CTA of K1 (one thread): this rank's p'Ap
-// partial into every rank's mailbox, then the flags.
-__device__ void dist_release_phase0(const DistDev& D, double pq_loc) {
-  const unsigned long long s = ld_volatile_u64(D.seq);
-  const int par = (int)((s + 1) & 1);
-  for (int q = 0; q < D.nranks; ++q) D.pmbox[q][mbox_index(0, par, D.rank, 0)] = pq_loc;
-  dist_release(D, 0, s + 1);
-  D.seq[0] = s + 1;
-}
 
 }  // namespace
 }  // namespace sbx

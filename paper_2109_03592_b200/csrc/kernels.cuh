@@ -76,8 +76,16 @@ struct CgScalars {
   double pq_loc, rz_loc, rr_loc;  // this rank's partials (distributed)
   // single-graph solve: what the device prologue found (kPre* bits)
   int32_t pre;
-  int32_t pad_;
+  // distributed: the update kernel left this rank's r'z / r'r partials in
+  // rz_loc / rr_loc; the next K1 exchanges them and takes the scalar step
+  int32_t xpend;
   double mu;  // pressure CG: mean of r/diag (the deflated preconditioner)
+  // distributed: the residual history (the scalar step runs in K1) and a
+  // marker for a K1 that only found the solve finished (timing mode)
+  double* hist;
+  int64_t hist_cap;
+  int32_t k1_idle;
+  int32_t pad_;
 };
 // A batched solve of up to kMaxComp right-hand sides with one operator (the
 // three velocity components of FlowSolver::solve_velocity_star,

@@ -7,10 +7,10 @@ import glob
 import statistics
 import sys
 
-SEG = [("K1 (CTA0 start -> last CTA)", 0, 1), ("K1 end -> K2 start", 1, 2),
-       ("K2: wait for peers", 2, 3), ("interface groups + grid barrier", 3, 4),
-       ("K2 body (-> last CTA)", 4, 5), ("r'z/r'r exchange", 5, 6),
-       ("exchange -> next K1 start", 6, 7)]
+SEG = [("K1 head: r'z/r'r exchange + step", 0, 6), ("K1 body (-> last CTA)", 6, 1),
+       ("K1 end -> K2 start", 1, 2), ("K2: release + wait for peers", 2, 3),
+       ("interface groups + grid barrier", 3, 4), ("K2 body (-> last CTA)", 4, 5),
+       ("K2 last CTA -> next K1 start", 5, 7)]
 SEG1 = [("K1 (CTA0 start -> last CTA)", 0, 1), ("K1 end -> K2 start", 1, 4),
         ("K2 body (-> last CTA)", 4, 5), ("K2 last CTA -> next K1 start", 5, 8)]
 
