@@ -564,6 +564,12 @@ __global__ void __launch_bounds__(AxCfg<n>::threads)
 // step.  The group width is the smallest multiple of 32 (<= 192) that leaves at
 // most 1/8 of the lanes idle, else the plain round-up (n = 6: 160 threads for
 // 4 elements instead of 64 threads with 28 idle).
+#ifndef SBX_K2_MAXT
+#define SBX_K2_MAXT 384  // consumer threads per K2 CTA at most (A/B knob)
+#endif
+#ifndef SBX_K2_MAXT6
+#define SBX_K2_MAXT6 512  // the same for n <= 6
+#endif
 #ifndef SBX_K2_MAXTG
 #define SBX_K2_MAXTG 192  // widest K2 group considered (A/B knob)
 #endif
@@ -621,7 +627,10 @@ struct K2Choice {
   static constexpr int pick() {
     for (int g = 16; g >= 1; --g) {
       if (g * T::TG + 32 > 1024) continue;
-      if (g * T::TG > 384) continue;  // ~150 registers per consumer thread
+      // ~150 registers per consumer thread; n <= 6 needs ~110 and gains from a
+      // third group (measured at 64^3 N=5: K2 0.61 -> 0.54 ms; at N=7 a wider
+      // CTA loses, 0.84 -> 1.01 ms)
+      if (g * T::TG > (n <= 6 ? SBX_K2_MAXT6 : SBX_K2_MAXT)) continue;
       if ((size_t)g * (2 * slot_bytes + group_bytes) <= BUDGET) return g;
     }
     return 1;
