@@ -30,6 +30,7 @@
 #include "ax_core.cuh"
 #include "ax_tma.cuh"
 #include "ax_dmma.cuh"
+#include "ax_dmma10.cuh"
 #include "cg.cuh"
 #include "dist_kern.cuh"
 #include "sbx_internal.h"
@@ -1273,6 +1274,41 @@ cudaError_t launch_k1_tma(const OpDev& op, const double* r, const double* dinv, 
   }
 }
 
+// K1 on the FP64 tensor cores at n = 10 (trilinear metric): ax_dmma10.cuh
+template <bool HAS_DINV, bool HAS_BM>
+cudaError_t launch_k1_dmma10(const OpDev& op, const double* r, const double* dinv, double* p,
+                             double* x, double* w, double h1, double h2, CgScalars* sc,
+                             double* partials, cudaStream_t s, int dev) {
+  using Pol = CgK1Pol<HAS_DINV, HAS_BM>;
+  using Ch = Dmma10Choice<Pol::NV, dmma10_ovl<Pol>()>;
+  if constexpr (!Ch::ok) {
+    return cudaErrorNotSupported;
+  } else {
+    using L = Dmma10Layout<Pol::NV, Ch::TEAMS, Ch::S, dmma10_ovl<Pol>()>;
+    auto kern = k1_dmma10_kernel<Pol, Ch::TEAMS, Ch::S>;
+    static std::atomic<bool> attr_set[64];
+    if (!attr_set[dev & 63]) {
+      cudaError_t err =
+          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::smem);
+      if (err != cudaSuccess) return err;
+      attr_set[dev & 63] = true;
+    }
+    DParam<10> Dp;
+    for (int q = 0; q < 100; ++q) Dp.d[q] = op.Dh[q];
+    QParam<10> Qp;
+    for (int q = 0; q < 10; ++q) {
+      Qp.x[q] = op.Xh[q];
+      Qp.w[q] = op.Wh[q];
+    }
+    typename Pol::Args a{r, dinv, p, x, w, op.bm, h2, sc, op.dd, 0.0, 0.0, 0, 0, nullptr, 0};
+    a.multi = t_multi;
+    int64_t grid = num_sms(dev);
+    if (grid > op.E) grid = op.E;
+    return launch_pdl(kern, dim3((unsigned)grid, t_ncomp), L::threads, L::smem, s, a, op.tl,
+                      op.E, h1, Dp, partials, Qp);
+  }
+}
+
 // K1 on the FP64 tensor cores (n = 8, trilinear metric): ax_dmma.cuh
 template <bool HAS_DINV, bool HAS_BM>
 cudaError_t launch_k1_dmma(const OpDev& op, const double* r, const double* dinv, double* p,
@@ -1351,6 +1387,18 @@ cudaError_t launch_k1(const OpDev& op, const double* r, const double* dinv, doub
           e = launch_k1_dmma<true, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
         else
           e = launch_k1_dmma<false, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
+      }
+    }
+    if constexpr (n == 10) {
+      if (tri && !fma_k1) {
+        if (dinv && h2 != 0.0)
+          e = launch_k1_dmma10<true, true>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
+        else if (h2 != 0.0)
+          e = launch_k1_dmma10<false, true>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
+        else if (dinv)
+          e = launch_k1_dmma10<true, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
+        else
+          e = launch_k1_dmma10<false, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
       }
     }
     if (tri && e == cudaErrorNotSupported) e = go(std::true_type{});
