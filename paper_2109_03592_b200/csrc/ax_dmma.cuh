@@ -187,6 +187,7 @@ __global__ void __launch_bounds__(DmmaLayout<Pol::NV, GROUPS, NSLOT>::threads, 1
   if (!Pol::init_scalars(args_l)) {
     if (SBX_DMMA_SELF && threadIdx.x == kIssuer)
       for (int64_t m = 0; m < M && m < S; ++m) mbar_wait(&full[m], 0u);
+    Pol::finish(args_l, 0.0, partials, red_sm, &last_flag);  // (the ticket records why)
     return;
   }
   if (!SBX_DMMA_SELF && warp == GROUPS) {

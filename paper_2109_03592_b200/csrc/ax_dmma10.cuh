@@ -157,6 +157,7 @@ __global__ void __launch_bounds__(Dmma10Layout<Pol::NV, TEAMS, NSLOT, dmma10_ovl
   if (!Pol::init_scalars(args_l)) {
     if (threadIdx.x == kIssuer)
       for (int64_t m = 0; m < M && m < S; ++m) mbar_wait(&full[m], 0u);
+    Pol::finish(args_l, 0.0, partials, red_sm, &last_flag);  // (the ticket records why)
     return;
   }
 

@@ -117,7 +117,8 @@ struct CgK1Pol {
   // init_scalars: the scalars of this iteration (multi-GPU: after the
   // previous iteration's r'z / r'r exchange), false when the exchange found
   // the solve finished
-  __device__ static bool init(Args& a) { return init_ptrs(a) && init_scalars(a); }
+  // (a false init_scalars -- the multi-GPU head found the solve finished --
+  // still takes the kernel's ticket: the caller runs finish() with red = 0)
   __device__ static bool init_ptrs(Args& a) {
     if (a.multi) {
       const int c = blockIdx.y;
@@ -228,6 +229,10 @@ __device__ void CgK1Pol<HAS_DINV, HAS_BM>::finish(const Args& a, double red, dou
     sc->counter[0] = 0;
     // every CTA has read the scalars: record the step taken at the head
     if (dist_step_smem().pending) dist_step_commit(sc, dist_step_smem());
+    if (sc->done) {  // the head found the solve finished: no iteration ran
+      sc->k1_idle = 1;
+      return;
+    }
     sc->pq_loc = tot;  // published and summed over ranks by k2_dist_prologue
     trace_stamp(a.dd, sc->it, 1);
     a.dd->seq[0] += 1;  // phase 0 of this iteration: released by the update kernel

@@ -419,8 +419,11 @@ __device__ __forceinline__ void dist_step_commit(CgScalars* __restrict__ sc, con
 // left r'z / r'r partials (sc->xpend), publish this rank's (block 0: phase-1
 // mailboxes + release), wait for every peer's, sum in rank order and take the
 // scalar step.  Returns 0: no step pending (first iteration), 1: stepped,
-// iterate; 2: the solve is finished (recorded by block 0; the update kernel
-// that follows sees done and ends the graph loop).
+// iterate; 2: the solve is finished.  Nothing here writes the scalars: every
+// CTA reads them at its start, so they change only in the last CTA of the
+// kernel (its ticket follows every CTA's head), which records the step --
+// also when the solve is finished and the CTAs skip the iteration; the
+// update kernel that follows then sees done and ends the graph loop.
 __device__ int k1_dist_head(const DistDev& D, CgScalars* __restrict__ sc) {
   __shared__ int res;
   DistStep& st = dist_step_smem();
@@ -480,10 +483,6 @@ __device__ int k1_dist_head(const DistDev& D, CgScalars* __restrict__ sc) {
       o.pending = 1;
       st = o;
       r = o.done ? 2 : 1;
-      if (r == 2 && lead) {
-        dist_step_commit(sc, o);
-        sc->k1_idle = 1;
-      }
     }
     res = r;
   }

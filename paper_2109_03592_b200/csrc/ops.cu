@@ -120,7 +120,8 @@ struct AxPol {
     double* w;
     double h2;
   };
-  __device__ static bool init(Args&) { return true; }
+  __device__ static bool init_ptrs(Args&) { return true; }
+  __device__ static bool init_scalars(Args&) { return true; }
   __device__ static double* partials_of(const Args&, double* partials) { return partials; }
   __device__ static const int32_t* send_index(const Args&) { return nullptr; }
   __device__ static void element_done(Args&, int, int64_t, int, int, int, int, int) {}
