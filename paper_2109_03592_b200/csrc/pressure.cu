@@ -36,6 +36,14 @@ namespace sbx {
 
 namespace {
 
+// one of three component pointers (a runtime index into a local pointer
+// array would put the array in local memory)
+template <class T>
+__device__ __forceinline__ T* pick3(T* a, T* b, T* c, int i) {
+  return i == 0 ? a : (i == 1 ? b : c);
+}
+
+
 constexpr int kPThreads = 128;
 
 // 1-D operators in device memory, staged into shared memory per CTA:
@@ -131,7 +139,6 @@ __global__ void __launch_bounds__(kPThreads)
   __syncthreads();
   const double* sIt = sM + PM::OFF_IT;
   const double* sCt = sM + PM::OFF_CT;
-  double* outs[3] = {g0, g1, g2};
   for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
     // per owned GL node: the operand p and the nine metric factors
     double pv[QPT], F[QPT][9];
@@ -206,7 +213,7 @@ __global__ void __launch_bounds__(kPThreads)
       }
       __syncthreads();
       // x pass: g = Cx B0 + Ix B12, written straight to global
-      double* out = outs[comp] + e * n3;
+      double* out = pick3(g0, g1, g2, comp) + e * n3;
       for (int idx = threadIdx.x; idx < n3; idx += blockDim.x) {
         const int ix = idx % n, kzjy = idx / n;
         const double* Ct = sCt + ix * m;
@@ -261,7 +268,6 @@ __global__ void __launch_bounds__(kPThreads)
   __syncthreads();
   const double* sI = sM + PM::OFF_I;
   const double* sCI = sM + PM::OFF_CI;
-  const double* ins[3] = {v0, v1, v2};
   double pq = 0.0;
   for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
     double acc[QPT], F[QPT][9];
@@ -275,7 +281,7 @@ __global__ void __launch_bounds__(kPThreads)
     }
     for (int comp = 0; comp < 3; ++comp) {
       __syncthreads();
-      const double* vin = ins[comp] + e * n3;
+      const double* vin = pick3(v0, v1, v2, comp) + e * n3;
       for (int idx = threadIdx.x; idx < n3; idx += blockDim.x) sV[idx] = vin[idx];
       __syncthreads();
       // x pass: X0 = CIx v, X12 = Ix v   ([k][j][a])
@@ -404,6 +410,17 @@ __global__ void __launch_bounds__(SBX_PENCIL_THREADS)
   double* sp = sF + S::F_D;  // [m3]
   double* sA = sp + S::P_D;  // [CP][3][n][m][m]  (kz, jj, ii)
   double* sB = sA + S::A_D;  // [CP][2][n][n][m]  (kz, jy, ii)
+  // GL nodes / weights in shared memory (compile-time indices into the
+  // parameter; a runtime index would copy it to local memory)
+  __shared__ double sGx[n], sGw[n];
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < m; ++q) {
+      sGx[q] = M.x[q];
+      sGw[q] = M.w[q];
+    }
+  }
+  __syncthreads();
   if (CG && cg.sc->done) return;
   double beta = 0.0, ap = 0.0, mu = 0.0;
   int first = 1;
@@ -413,12 +430,11 @@ __global__ void __launch_bounds__(SBX_PENCIL_THREADS)
     mu = cg.sc->mu;
     first = cg.sc->first;
   }
-  double* outs[3] = {g0, g1, g2};
   for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
     __syncthreads();
     for (int q = threadIdx.x; q < m3; q += blockDim.x) {
       double F[9];
-      gl_metric(TL + e * 24, M.x, M.w, q % m, (q / m) % m, q / m2, F);
+      gl_metric(TL + e * 24, sGx, sGw, q % m, (q / m) % m, q / m2, F);
 #pragma unroll
       for (int c = 0; c < 9; ++c) sF[c * m3 + q] = F[c];
       const int64_t a = e * m3 + q;
@@ -504,7 +520,7 @@ __global__ void __launch_bounds__(SBX_PENCIL_THREADS)
           b0[ii] = B[ii];
           b12[ii] = B[n * n * m + ii];
         }
-        double* out = outs[c0 + cl] + e * n3 + row * n;
+        double* out = pick3(g0, g1, g2, c0 + cl) + e * n3 + row * n;
 #pragma unroll
         for (int ix = 0; ix < n; ++ix) {
           double acc = 0.0;
@@ -544,14 +560,24 @@ __global__ void __launch_bounds__(SBX_PENCIL_THREADS)
   double* sX = sVb + S::V_D;  // [CP][2][n][n][m]   (k, j, a)
   double* sY = sX + S::X_D;  // [CP][3][n][m][m]   (k, b, a)
   double* sQ = sY + S::Y_D;  // [3][m3] per-component contributions
+  // GL nodes / weights in shared memory (compile-time indices into the
+  // parameter; a runtime index would copy it to local memory)
+  __shared__ double sGx[n], sGw[n];
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < m; ++q) {
+      sGx[q] = M.x[q];
+      sGw[q] = M.w[q];
+    }
+  }
+  __syncthreads();
   if (CG && sc->done) return;
-  const double* ins[3] = {v0, v1, v2};
   double pq = 0.0;
   // the three fields of an element, copied asynchronously one element ahead
   auto prefetch = [&](int64_t ee, double* dst) {
     if (ee < E)
       for (int q = threadIdx.x; q < 3 * n3; q += blockDim.x)
-        cp_async8(dst + q, ins[q / n3] + ee * n3 + q % n3, true);
+        cp_async8(dst + q, pick3(v0, v1, v2, q / n3) + ee * n3 + q % n3, true);
     cp_async_commit();
   };
   prefetch(blockIdx.x, sVb);
@@ -561,7 +587,7 @@ __global__ void __launch_bounds__(SBX_PENCIL_THREADS)
     prefetch(e + gridDim.x, sVb + (buf ^ 1) * 3 * n3);
     for (int q = threadIdx.x; q < m3; q += blockDim.x) {
       double F[9];
-      gl_metric(TL + e * 24, M.x, M.w, q % m, (q / m) % m, q / m2, F);
+      gl_metric(TL + e * 24, sGx, sGw, q % m, (q / m) % m, q / m2, F);
 #pragma unroll
       for (int c = 0; c < 9; ++c) sF[c * m3 + q] = F[c];
     }

@@ -280,7 +280,23 @@ __global__ void gs3_scale_box_kernel(BoxLat b, int n, int cols, double* __restri
 // Out of place: v_c = scale * gs_sum(g_c).  Every thread sums its own node's
 // copies (the same copies in the same reference order for every copy, so
 // every copy gets the same bits as the in-place kernel) -- no serial owner
-// loop, the partner loads of all copies in flight at once.
+// loop, the partner loads of all copies in flight at once.  The copies are the
+// product of at most two options per axis; with each axis's options in
+// ascending cell order, the (z, y, x) nesting visits them in ascending
+// element index -- the reference's order -- with compile-time indices only
+// (no local-memory index array, no sort).
+__device__ __forceinline__ Ax32 axis32_sorted(int g, int count, int N, bool per) {
+  Ax32 o = axis32(g, count, N, per);
+  if (o.cnt == 2 && o.cell[1] < o.cell[0]) {
+    const int c = o.cell[0], l = o.loc[0];
+    o.cell[0] = o.cell[1];
+    o.loc[0] = o.loc[1];
+    o.cell[1] = c;
+    o.loc[1] = l;
+  }
+  return o;
+}
+
 __global__ void gs3_scale_box_oop_kernel(BoxLat b, int n, int cols,
                                          const double* __restrict__ f0,
                                          const double* __restrict__ f1,
@@ -293,6 +309,9 @@ __global__ void gs3_scale_box_oop_kernel(BoxLat b, int n, int cols,
        col += gridDim.x * blockDim.x) {
     const Col32 c = col_of(b, n, col);
     const bool face = c.i == 0 || c.i == N || c.j == 0 || c.j == N;
+    // the x / y options are the column's, the same for every k
+    const Ax32 ox = axis32_sorted(gcoord(c.cx, c.i, b.ex, N, b.per[0]), b.ex, N, b.per[0]);
+    const Ax32 oy = axis32_sorted(gcoord(c.cy, c.j, b.ey, N, b.per[1]), b.ey, N, b.per[1]);
     for (int k = 0; k < n; ++k) {
       const int a = c.e * n3 + (k * n + c.j) * n + c.i;
       const double w = scale[a];
@@ -302,16 +321,25 @@ __global__ void gs3_scale_box_oop_kernel(BoxLat b, int n, int cols,
         v2[a] = __dmul_rn(f2[a], w);
         continue;
       }
-      int idx[8];
-      bool masked;
-      const int m = copies32(b, n, c, k, idx, masked);
+      const Ax32 oz = axis32_sorted(gcoord(c.cz, k, b.ez, N, b.per[2]), b.ez, N, b.per[2]);
       double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-      for (int q = 0; q < m; ++q) {
-        s0 = __dadd_rn(s0, f0[idx[q]]);
-        s1 = __dadd_rn(s1, f1[idx[q]]);
-        s2 = __dadd_rn(s2, f2[idx[q]]);
+#pragma unroll
+      for (int z = 0; z < 2; ++z) {
+#pragma unroll
+        for (int y = 0; y < 2; ++y) {
+#pragma unroll
+          for (int x = 0; x < 2; ++x) {
+            if (z < oz.cnt && y < oy.cnt && x < ox.cnt) {
+              const int e = ox.cell[x] + b.ex * (oy.cell[y] + b.ey * oz.cell[z]);
+              const int q = e * n3 + (oz.loc[z] * n + oy.loc[y]) * n + ox.loc[x];
+              s0 = __dadd_rn(s0, f0[q]);
+              s1 = __dadd_rn(s1, f1[q]);
+              s2 = __dadd_rn(s2, f2[q]);
+            }
+          }
+        }
       }
-      if (m == 1) {  // a singleton: gs leaves it alone (no 0.0 + x)
+      if (ox.cnt * oy.cnt * oz.cnt == 1) {  // a singleton: gs leaves it alone (no 0.0 + x)
         s0 = f0[a];
         s1 = f1[a];
         s2 = f2[a];
