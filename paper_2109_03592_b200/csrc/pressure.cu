@@ -379,6 +379,9 @@ __global__ void __launch_bounds__(kPThreads)
 // inputs in registers, the 1-D operator as compile-time constant-bank operands
 // (kernel parameters), every component of a pass in flight at once
 // (CP = 3) or one component per pass (CP = 1, less shared memory).
+#ifndef SBX_PENCIL_MINB
+#define SBX_PENCIL_MINB 1  // resident CTAs per SM the pencil kernels are compiled for (A/B knob)
+#endif
 #ifndef SBX_PENCIL_THREADS
 #define SBX_PENCIL_THREADS 192  // threads per CTA of the pencil kernels (A/B: 128 / 192 / 256 -> 14.2 / 13.7 / 18.0 ms per pressure iteration at 64^3)
 #endif
@@ -399,7 +402,7 @@ struct PGrad2 {
 };
 
 template <int n, int CP, bool CG>
-__global__ void __launch_bounds__(SBX_PENCIL_THREADS)
+__global__ void __launch_bounds__(SBX_PENCIL_THREADS, SBX_PENCIL_MINB)
     p_grad2_kernel(const double* __restrict__ pin, int64_t E, const double* __restrict__ TL,
                    PMatK<n> M, double* __restrict__ g0, double* __restrict__ g1,
                    double* __restrict__ g2, PCgArgs cg) {
@@ -545,7 +548,7 @@ struct PDiv2 {
 };
 
 template <int n, int CP, bool CG>
-__global__ void __launch_bounds__(SBX_PENCIL_THREADS)
+__global__ void __launch_bounds__(SBX_PENCIL_THREADS, SBX_PENCIL_MINB)
     p_div2_kernel(const double* __restrict__ v0, const double* __restrict__ v1,
                   const double* __restrict__ v2, int64_t E, const double* __restrict__ TL,
                   PMatK<n> M, double* __restrict__ qout, const double* __restrict__ pdot,
