@@ -127,10 +127,13 @@ constexpr int kMaxRanks = 8;
 // CG loop, 1 r'z/r'r, 2 standalone gather-scatter halo, 3 setup reductions.
 // The halo is PUSHED: a sender stores its interface copy values into each
 // neighbour's receive buffer over NVLink as soon as they are computed (the
-// K1 epilogue), fences them at system scope once per thread, and releases its
-// flag; the receiver then reads only local memory.  Parity = sequence number & 1: a peer can run at most
-// one use of a phase ahead (it needs this rank's flag of the previous use), so
-// double buffering makes every access race-free.
+// K1 epilogue); the next kernel (K2), once K1 has completed, releases the
+// phase with one system fence and relaxed flag stores; the receiver then
+// reads only local memory.  The r'z / r'r partials of K2 are released by the
+// next K1's head.  Parity = sequence number & 1: a peer can run at most one
+// use of a phase ahead (it needs this rank's flag of the previous use, and a
+// kernel starts only after its predecessor -- the last reader of the other
+// parity -- has completed), so double buffering makes every access race-free.
 constexpr size_t kWinFlags = 0, kWinMbox = 256, kWinRecv = 2304;
 
 __host__ __device__ constexpr int mbox_index(int phase, int par, int src, int c) {
