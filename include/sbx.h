@@ -160,6 +160,17 @@ sbx_status sbx_ctx_set_stream(sbx_ctx* ctx, void* stream);
 
 /* ------------------------------------------------------------ operators --- */
 
+/* Per-node Helmholtz coefficients (HelmholtzCoeffs::h1_field / h2_field,
+ * operators.hpp:42-43): E*n^3 fields (host or device pointers, copied into the
+ * context) that replace the scalar h1 / h2 in every later axhelm,
+ * axhelm_diagonal, apply and pcg on this context, read at each node where
+ * operators.cpp:242, 258, 292-293 read them; NULL restores the scalar.  With
+ * fields the operators and the solve run in the reference evaluation order in
+ * either mode (the fused FAST kernels take scalars).  Single-process contexts;
+ * h2 fields need bm. */
+sbx_status sbx_ctx_set_coeff_fields(sbx_ctx* ctx, const double* h1_field,
+                                    const double* h2_field);
+
 /* axhelm (operators.hpp:59-60, operators.cpp:215-263): w = D^T G D u h1 + h2 bm u */
 sbx_status sbx_axhelm(sbx_ctx* ctx, const double* u, double* w, double h1, double h2,
                       uint32_t flags);

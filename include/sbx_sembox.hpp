@@ -104,6 +104,7 @@ class Device {
               bool exact = false) const {
     shape(u);
     if (!out.same_shape(u)) out = sembox::Field(u.tag, u.elem_count, u.n1d);
+    fields(c);
     check(sbx_axhelm(ctx_, u.v.data(), out.v.data(), c.h1, c.h2, exact ? SBX_FLAG_EXACT : 0));
   }
 
@@ -118,6 +119,7 @@ class Device {
     return [this, c, exact](const sembox::Field& x, sembox::Field& y) {
       shape(x);
       if (!y.same_shape(x)) y = sembox::Field(x.tag, x.elem_count, x.n1d);
+      fields(c);
       check(sbx_apply(ctx_, x.v.data(), y.v.data(), c.h1, c.h2, exact ? SBX_FLAG_EXACT : 0));
     };
   }
@@ -134,6 +136,7 @@ class Device {
   // Jacobi on HelmholtzOperator::assembled_diagonal (stepper.cpp:175-186)
   sembox::PrecondFn jacobi_fn(sembox::HelmholtzCoeffs c) const {
     auto diag = std::make_shared<sembox::Field>(sembox::GridTag::velocity, elems_, n1d_);
+    fields(c);
     check(sbx_axhelm_diagonal(ctx_, c.h1, c.h2, 1, diag->v.data()));
     return [diag](const sembox::Field& r, sembox::Field& z) {
       if (!z.same_shape(r)) z = sembox::Field(r.tag, r.elem_count, r.n1d);
@@ -160,6 +163,7 @@ class Device {
     cfg.history = hist.data();
     cfg.history_capacity = (int64_t)hist.size();
     sbx_pcg_result r{};
+    fields(c);
     check(sbx_pcg(ctx_, b.v.data(), x.v.data(), &cfg, &r), r.error_iteration);
     sembox::PcgResult out;
     out.iterations = r.iterations;
@@ -172,6 +176,19 @@ class Device {
   }
 
  private:
+  // HelmholtzCoeffs::h1_field / h2_field (operators.hpp:42-43) onto the
+  // context (sbx_ctx_set_coeff_fields) whenever a call carries them (their values
+  // may have changed) or the context still holds earlier ones
+  void fields(const sembox::HelmholtzCoeffs& c) const {
+    const double* f1 = c.h1_field ? c.h1_field->v.data() : nullptr;
+    const double* f2 = c.h2_field ? c.h2_field->v.data() : nullptr;
+    if (f1 == f1_ && f2 == f2_ && !f1 && !f2) return;
+    check(sbx_ctx_set_coeff_fields(ctx_, f1, f2));
+    f1_ = f1;
+    f2_ = f2;
+  }
+  mutable const double* f1_ = nullptr;
+  mutable const double* f2_ = nullptr;
   void shape(const sembox::Field& f) const {
     if (f.tag != sembox::GridTag::velocity || f.elem_count != elems_ || f.n1d != n1d_)
       throw sembox::ContractViolation("sbx: field grid/shape mismatch");

@@ -136,6 +136,7 @@ def _ref():
         L.ref_copy_int64.argtypes = [_P, C.c_int, _i64p]
         L.ref_copy_mult.argtypes = [_P, _i32p]
         L.ref_axhelm.argtypes = [_P, _dp, C.c_double, C.c_double, C.c_int, _dp]
+        L.ref_set_coeff_fields.argtypes = [_P, C.c_void_p, C.c_void_p]
         L.ref_axhelm_diagonal.argtypes = [_P, C.c_double, C.c_double, C.c_int, _dp]
         L.ref_gs_sum.argtypes = [_P, _dp]
         L.ref_apply.argtypes = [_P, C.c_double, C.c_double, C.c_int, _dp, _dp]
@@ -299,6 +300,16 @@ class Problem:
     # -- operators --------------------------------------------------------
     def _gargs(self):
         return (self.deriv, self.g1, self.g2, self.g3, self.g4, self.g5, self.g6, self.bm)
+
+    def set_coeff_fields(self, h1f=None, h2f=None):
+        """HelmholtzCoeffs::h1_field / h2_field (operators.hpp:42-43) for every
+        later operator and pcg of this (reference-backed) problem; None: the
+        scalar."""
+        assert self.backend == "ref", "per-node coefficients: reference backend only"
+        self._cf = [None if f is None else np.ascontiguousarray(f, np.float64)
+                    for f in (h1f, h2f)]
+        _ref().ref_set_coeff_fields(self._h, *[None if f is None else f.ctypes.data
+                                               for f in self._cf])
 
     def axhelm(self, u, h1=1.0, h2=0.0, flip=False):
         u = np.ascontiguousarray(u, np.float64)

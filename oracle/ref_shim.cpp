@@ -71,7 +71,15 @@ struct Problem {
   PressureBasis pb;
   PressureGeometry pg;
   Field inv_bdiag, pdiag;
+  // per-node Helmholtz coefficients (HelmholtzCoeffs::h1_field / h2_field,
+  // operators.hpp:42-43), applied by every operator below when set
+  Field h1f, h2f;
+  bool has_h1f = false, has_h2f = false;
 };
+
+HelmholtzCoeffs coeffs_of(const Problem& p, double h1, double h2) {
+  return {h1, h2, p.has_h1f ? &p.h1f : nullptr, p.has_h2f ? &p.h2f : nullptr};
+}
 
 // FlowSolver::apply_pressure_operator (stepper.cpp:240-248), restated with the
 // reference's own operators (stepper.cpp itself cannot be linked: it needs
@@ -238,12 +246,21 @@ void ref_copy_mult(void* h, std::int32_t* out) {
   std::memcpy(out, p->map.mult.data(), p->map.mult.size() * sizeof(std::int32_t));
 }
 
+// h1f / h2f: E*n^3 per-node coefficients, or NULL for the scalar
+void ref_set_coeff_fields(void* h, const double* h1f, const double* h2f) {
+  auto* p = static_cast<Problem*>(h);
+  p->has_h1f = h1f != nullptr;
+  p->has_h2f = h2f != nullptr;
+  if (h1f) p->h1f = wrap(*p, h1f);
+  if (h2f) p->h2f = wrap(*p, h2f);
+}
+
 int ref_axhelm(void* h, const double* u, double h1, double h2, int flip, double* out) {
   auto* p = static_cast<Problem*>(h);
   return guarded([&] {
     debug::axhelm_sign_flip.store(flip != 0);
     Field uf = wrap(*p, u), of;
-    HelmholtzCoeffs hc{h1, h2, nullptr, nullptr};
+    HelmholtzCoeffs hc = coeffs_of(*p, h1, h2);
     try {
       axhelm(uf, hc, p->gf, p->basis, of);
     } catch (...) {
@@ -258,7 +275,7 @@ int ref_axhelm(void* h, const double* u, double h1, double h2, int flip, double*
 int ref_axhelm_diagonal(void* h, double h1, double h2, int assembled, double* out) {
   auto* p = static_cast<Problem*>(h);
   return guarded([&] {
-    HelmholtzOperator op{&p->gf, &p->basis, &p->map, &p->mask, {h1, h2, nullptr, nullptr}};
+    HelmholtzOperator op{&p->gf, &p->basis, &p->map, &p->mask, coeffs_of(*p, h1, h2)};
     const Field d = assembled ? op.assembled_diagonal()
                               : axhelm_diagonal(op.coeffs, p->gf, p->basis);
     unwrap(d, out);
@@ -278,7 +295,7 @@ int ref_apply(void* h, double h1, double h2, int use_mask, const double* x, doub
   auto* p = static_cast<Problem*>(h);
   return guarded([&] {
     HelmholtzOperator op{&p->gf, &p->basis, &p->map, use_mask ? &p->mask : nullptr,
-                         {h1, h2, nullptr, nullptr}};
+                         coeffs_of(*p, h1, h2)};
     Field xf = wrap(*p, x), of(GridTag::velocity, p->mesh.elem_count, p->basis.n());
     op.apply(xf, of);
     unwrap(of, out);
@@ -304,7 +321,7 @@ int ref_pcg(void* h, double h1, double h2, int precond, const double* b, double*
   info[2] = -1;
   *hist_len = 0;
   return guarded([&] {
-    HelmholtzOperator op{&p->gf, &p->basis, &p->map, &p->mask, {h1, h2, nullptr, nullptr}};
+    HelmholtzOperator op{&p->gf, &p->basis, &p->map, &p->mask, coeffs_of(*p, h1, h2)};
     const Field diag = op.assembled_diagonal();
     const DotFn dot = [&](const Field& a, const Field& bb) {
       return field_dot_weighted(a, bb, p->map.inv_mult);
@@ -346,7 +363,7 @@ int ref_pcg(void* h, double h1, double h2, int precond, const double* b, double*
 int ref_bench_prepare(void* h, double h1, double h2, const double* b) {
   auto* p = static_cast<Problem*>(h);
   return guarded([&] {
-    HelmholtzOperator op{&p->gf, &p->basis, &p->map, &p->mask, {h1, h2, nullptr, nullptr}};
+    HelmholtzOperator op{&p->gf, &p->basis, &p->map, &p->mask, coeffs_of(*p, h1, h2)};
     p->bench_diag = op.assembled_diagonal();
     p->bench_b = wrap(*p, b);
     p->bench_x = Field(GridTag::velocity, p->mesh.elem_count, p->basis.n());

@@ -76,6 +76,7 @@ _sig("sbx_ctx_copy_array", _i, _vp, _i, _vp)
 _sig("sbx_ctx_set_stream", _i, _vp, _vp)
 _sig("sbx_ctx_features", _i, _vp, C.POINTER(_u32))
 _sig("sbx_axhelm", _i, _vp, _vp, _vp, _d, _d, _u32)
+_sig("sbx_ctx_set_coeff_fields", _i, _vp, _vp, _vp)
 _sig("sbx_axhelm_diagonal", _i, _vp, _d, _d, _i, _vp)
 _sig("sbx_gs_sum", _i, _vp, _vp)
 _sig("sbx_apply", _i, _vp, _vp, _vp, _d, _d, _u32)

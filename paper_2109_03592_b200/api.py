@@ -16,6 +16,7 @@ the context) or CUDA float64 torch tensors (device, zero-copy).
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 from dataclasses import dataclass, field
 from typing import Optional
@@ -260,10 +261,33 @@ def build_dirichlet_mask(mesh: HexMesh, degree: int) -> np.ndarray:
 # --------------------------------------------------------------- operator --
 @dataclass
 class HelmholtzCoeffs:
-    """operators.hpp:39-44 (scalar h1, h2)"""
+    """operators.hpp:39-44: scalar h1, h2, or per-node fields h1_field /
+    h2_field (E*n^3 arrays, host or device; they replace the scalar at each
+    node, operators.cpp:242, 258, 292-293)."""
 
     h1: float = 1.0
     h2: float = 0.0
+    h1_field: Optional[object] = None
+    h2_field: Optional[object] = None
+
+
+@contextlib.contextmanager
+def _coeff_fields(ctx, coeffs: HelmholtzCoeffs):
+    """Per-node coefficients on the context for the duration of one call
+    (sbx_ctx_set_coeff_fields)."""
+    f1, f2 = coeffs.h1_field, coeffs.h2_field
+    if f1 is None and f2 is None:
+        yield
+        return
+    f1 = None if f1 is None else _f64(f1)
+    f2 = None if f2 is None else _f64(f2)
+    ctx._shape_check(*[f for f in (f1, f2) if f is not None])
+    _check(lib.sbx_ctx_set_coeff_fields(ctx.handle, _ptr(f1) if f1 is not None else None,
+                                        _ptr(f2) if f2 is not None else None))
+    try:
+        yield
+    finally:
+        lib.sbx_ctx_set_coeff_fields(ctx.handle, None, None)
 
 
 @dataclass
@@ -412,7 +436,8 @@ def axhelm(u, coeffs: HelmholtzCoeffs, ctx: Context, out=None, exact=False, flip
     if out is None:
         out = np.empty(ctx.nodes) if isinstance(u, np.ndarray) else u.new_empty(ctx.nodes)
     flags = (L.FLAG_EXACT if exact else 0) | (L.FLAG_FLIP_T if flip else 0)
-    _check(lib.sbx_axhelm(ctx.handle, _ptr(u), _ptr(out), coeffs.h1, coeffs.h2, flags))
+    with _coeff_fields(ctx, coeffs):
+        _check(lib.sbx_axhelm(ctx.handle, _ptr(u), _ptr(out), coeffs.h1, coeffs.h2, flags))
     return out
 
 
@@ -431,7 +456,9 @@ def debug_cg_k1(u, coeffs: HelmholtzCoeffs, ctx: Context, out=None):
 def axhelm_diagonal(coeffs: HelmholtzCoeffs, ctx: Context, assembled=False, device=False):
     """operators.hpp:64-66 / operators.cpp:272-298 (+ gs_sum when assembled)."""
     out = ctx.new_field(device)
-    _check(lib.sbx_axhelm_diagonal(ctx.handle, coeffs.h1, coeffs.h2, int(assembled), _ptr(out)))
+    with _coeff_fields(ctx, coeffs):
+        _check(lib.sbx_axhelm_diagonal(ctx.handle, coeffs.h1, coeffs.h2, int(assembled),
+                                       _ptr(out)))
     return out
 
 
@@ -480,8 +507,9 @@ class HelmholtzOperator:
         x = _f64(x)
         self.ctx._shape_check(x, out)
         flags = (L.FLAG_EXACT if self.exact else 0) | (0 if self.use_mask else L.FLAG_NO_MASK)
-        _check(lib.sbx_apply(self.ctx.handle, _ptr(x), _ptr(out), self.coeffs.h1,
-                             self.coeffs.h2, flags))
+        with _coeff_fields(self.ctx, self.coeffs):
+            _check(lib.sbx_apply(self.ctx.handle, _ptr(x), _ptr(out), self.coeffs.h1,
+                                 self.coeffs.h2, flags))
         return out
 
     __call__ = apply
@@ -518,7 +546,8 @@ def pcg(op: HelmholtzOperator, b, x, cfg: KrylovConfig = KrylovConfig(),
         c.history = hist.ctypes.data
         c.history_capacity = hist.size
     r = L.PcgResultC()
-    rc = lib.sbx_pcg(op.ctx.handle, _ptr(b), _ptr(x), C.byref(c), C.byref(r))
+    with _coeff_fields(op.ctx, op.coeffs):
+        rc = lib.sbx_pcg(op.ctx.handle, _ptr(b), _ptr(x), C.byref(c), C.byref(r))
     _check(rc, r.error_iteration)
     out = PcgResult(r.iterations, r.rel_residual, r.rel_residual_precond, bool(r.converged))
     if hist is not None:
@@ -731,7 +760,8 @@ def pcg_multi(op: HelmholtzOperator, bs, xs, cfg: KrylovConfig = KrylovConfig(),
     res = (L.PcgResultC * count)()
     barr = (C.c_void_p * count)(*[_ptr(b) for b in bs])
     xarr = (C.c_void_p * count)(*[_ptr(x) for x in xs])
-    rc = lib.sbx_pcg_multi(op.ctx.handle, count, barr, xarr, C.byref(c), res)
+    with _coeff_fields(op.ctx, op.coeffs):
+        rc = lib.sbx_pcg_multi(op.ctx.handle, count, barr, xarr, C.byref(c), res)
     err_it = max((r.error_iteration for r in res), default=-1)
     _check(rc, err_it)
     out = []

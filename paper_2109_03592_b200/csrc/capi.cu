@@ -69,6 +69,8 @@ struct sbx_ctx {
   double* ddiag = nullptr;
   double* ddinv = nullptr;
   double diag_h1 = NAN, diag_h2 = NAN;
+  double* h1f = nullptr;  // per-node coefficients (sbx_ctx_set_coeff_fields)
+  double* h2f = nullptr;
   // fast CG
   std::unique_ptr<CgEngine> cg;
   // consistent-Poisson pressure operator (built on first use)
@@ -932,6 +934,36 @@ sbx_status sbx_ctx_copy_array(const sbx_ctx* c, int which, double* out) {
   }
 }
 
+sbx_status sbx_ctx_set_coeff_fields(sbx_ctx* c, const double* h1f, const double* h2f) {
+  SBX_TRY(check_ctx(c));
+  if (c->dist && (h1f || h2f)) {
+    set_error("sbx_ctx_set_coeff_fields: per-node coefficients are single-process only");
+    return SBX_E_CONFIG;
+  }
+  if (h2f && !c->op.bm) {
+    set_error("sbx_ctx_set_coeff_fields: h2 fields need the mass factors (bm)");
+    return SBX_E_SHAPE;
+  }
+  SBX_TRY(enter(c));
+  const size_t bytes = sizeof(double) * (size_t)c->op.nodes;
+  auto put = [&](const double* src, double** dst) -> sbx_status {
+    if (!src) return SBX_OK;
+    if (!*dst) {
+      void* p = nullptr;
+      SBX_TRY(dalloc(c, &p, bytes));
+      *dst = static_cast<double*>(p);
+    }
+    SBX_CUDA(cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyDefault, c->stream));
+    return SBX_OK;
+  };
+  SBX_TRY(put(h1f, &c->h1f));
+  SBX_TRY(put(h2f, &c->h2f));
+  c->op.h1f = h1f ? c->h1f : nullptr;
+  c->op.h2f = h2f ? c->h2f : nullptr;
+  c->diag_h1 = c->diag_h2 = NAN;  // the cached Jacobi diagonal no longer applies
+  return finish(c);
+}
+
 sbx_status sbx_axhelm(sbx_ctx* c, const double* u, double* w, double h1, double h2,
                       uint32_t flags) {
   SBX_TRY(check_ctx(c));
@@ -1092,7 +1124,10 @@ sbx_status sbx_pcg(sbx_ctx* c, const double* b, double* x, const sbx_pcg_config*
     set_error("distributed context used before sbx_ctx_dist_connect");
     return SBX_E_COMM;
   }
-  if (cfg->mode == SBX_MODE_FAST) {
+  // per-node coefficients: the fused kernels take scalars only, so the solve
+  // runs in the reference order (still on the device)
+  const bool fields = c->op.h1f || c->op.h2f;
+  if (cfg->mode == SBX_MODE_FAST && !fields) {
     if (cfg->precond == SBX_PRECOND_JACOBI) SBX_TRY(ensure_diag(c, cfg->h1, cfg->h2));
     CgRun run;
     run.op = &c->op;
@@ -1473,9 +1508,9 @@ sbx_status sbx_pcg_multi(sbx_ctx* c, int count, const double* const* b, double* 
     if (cfg->history) cq.history = cfg->history + (size_t)q * cfg->history_capacity;
     return sbx_pcg(c, b[q], x[q], &cq, &res[q]);
   };
-  if (cfg->mode != SBX_MODE_FAST || c->dist || count == 1) {
-    // reference order (or one rhs): the components one after the other, as
-    // solve_velocity_star does
+  if (cfg->mode != SBX_MODE_FAST || c->dist || count == 1 || c->op.h1f || c->op.h2f) {
+    // reference order (or one rhs, or per-node coefficients): the components
+    // one after the other, as solve_velocity_star does
     for (int q = 0; q < count; ++q) SBX_TRY(one(q));
     return SBX_OK;
   }

@@ -45,6 +45,10 @@ struct OpDev {
   // (see trilinear_coeffs) and the GLL nodes / weights, so the fused CG
   // kernel can form the metric at each node instead of streaming G
   const double* tl = nullptr;
+  // per-node Helmholtz coefficients (HelmholtzCoeffs::h1_field / h2_field,
+  // operators.hpp:42-43; sbx_ctx_set_coeff_fields), or null: the scalars
+  const double* h1f = nullptr;
+  const double* h2f = nullptr;
   const double* corners = nullptr;  // [E][8][3] (box / verified-hint contexts)
   double Xh[33], Wh[33];
   // lattice gather-scatter: mask / multiplicities / gs / rhs check derived

@@ -63,10 +63,13 @@ __global__ void __launch_bounds__(AxCfg<n>::threads)
 
 // Runtime-n fallback for 16 <= N <= 32 (n > 16): one element per CTA, every
 // thread loops over nodes; reference evaluation order in both modes.
+// Also the kernel for per-node coefficients h1f / h2f (any n): h1 and h2 read
+// at each node exactly where operators.cpp:242, 258 read them.
 __global__ void ax_generic_kernel(const double* __restrict__ u, const double* __restrict__ G,
                                   const double* __restrict__ bm, const double* __restrict__ D,
                                   double* __restrict__ w, int n, double h1, double h2,
-                                  double tsign) {
+                                  double tsign, const double* __restrict__ h1f = nullptr,
+                                  const double* __restrict__ h2f = nullptr) {
   extern __shared__ double sm[];
   const int n3 = n * n * n;
   double* su = sm;
@@ -88,9 +91,10 @@ __global__ void ax_generic_kernel(const double* __restrict__ u, const double* __
     }
     const double g1 = Ge[a], g2 = Ge[n3 + a], g3 = Ge[2 * n3 + a], g4 = Ge[3 * n3 + a],
                  g5 = Ge[4 * n3 + a], g6 = Ge[5 * n3 + a];
-    sr[a] = dmul(dadd(dadd(dmul(g1, r), dmul(g4, s)), dmul(g5, t)), h1);
-    ss[a] = dmul(dadd(dadd(dmul(g2, s), dmul(g4, r)), dmul(g6, t)), h1);
-    st[a] = dmul(dadd(dadd(dmul(g3, t), dmul(g5, r)), dmul(g6, s)), h1);
+    const double hh = h1f ? h1f[base + a] : h1;
+    sr[a] = dmul(dadd(dadd(dmul(g1, r), dmul(g4, s)), dmul(g5, t)), hh);
+    ss[a] = dmul(dadd(dadd(dmul(g2, s), dmul(g4, r)), dmul(g6, t)), hh);
+    st[a] = dmul(dadd(dadd(dmul(g3, t), dmul(g5, r)), dmul(g6, s)), hh);
   }
   __syncthreads();
   for (int a = threadIdx.x; a < n3; a += blockDim.x) {
@@ -102,7 +106,7 @@ __global__ void ax_generic_kernel(const double* __restrict__ u, const double* __
       const double t3 = dmul(dmul(tsign, D[l * n + k]), st[(l * n + j) * n + i]);
       acc = dadd(acc, dadd(dadd(t1, t2), t3));
     }
-    const double hb = bm ? dmul(h2, bm[base + a]) : 0.0;
+    const double hb = bm ? dmul(h2f ? h2f[base + a] : h2, bm[base + a]) : 0.0;
     w[base + a] = dadd(acc, dmul(hb, su[a]));
   }
 }
@@ -250,7 +254,8 @@ cudaError_t launch_ax_t(const OpDev& op, const double* u, double* w, double h1, 
 // ---- axhelm diagonal (operators.cpp:272-298), reference order -------------
 __global__ void ax_diag_kernel(const double* __restrict__ G, const double* __restrict__ bm,
                                const double* __restrict__ D, int n, int64_t nodes, double h1,
-                               double h2, double* __restrict__ diag) {
+                               double h2, double* __restrict__ diag,
+                               const double* __restrict__ h1f, const double* __restrict__ h2f) {
   const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (a >= nodes) return;
   const int n3 = n * n * n;
@@ -268,7 +273,7 @@ __global__ void ax_diag_kernel(const double* __restrict__ G, const double* __res
   s = dadd(s, dmul(dmul(dmul(2.0, D[i * n + i]), D[k * n + k]), Ge[4 * n3 + loc]));
   s = dadd(s, dmul(dmul(dmul(2.0, D[j * n + j]), D[k * n + k]), Ge[5 * n3 + loc]));
   const double b = bm ? bm[a] : 0.0;
-  diag[a] = dadd(dmul(h1, s), dmul(h2, b));
+  diag[a] = dadd(dmul(h1f ? h1f[a] : h1, s), dmul(h2f ? h2f[a] : h2, b));
 }
 
 // ---- gather-scatter over the boundary CSR (gather.cpp:85-98) --------------
@@ -434,15 +439,15 @@ cudaError_t launch_axhelm(const OpDev& op, const double* u, double* w, double h1
   const double tsign = flip ? -1.0 : 1.0;
   if (op.E == 0) return cudaSuccess;
   const int N = op.n - 1;
-  if (N > kMaxTemplN) {
+  if (N > kMaxTemplN || op.h1f || op.h2f) {  // (per-node coefficients: the reference order)
     const int n3 = op.n * op.n * op.n;
     const size_t smem = (size_t)4 * n3 * sizeof(double);
     cudaError_t err = cudaFuncSetAttribute(
         ax_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
-    const double* bm = (exact || h2 != 0.0) ? op.bm : nullptr;
+    const double* bm = (exact || h2 != 0.0 || op.h2f) ? op.bm : nullptr;
     ax_generic_kernel<<<(unsigned)op.E, 256, smem, s>>>(u, op.G, bm, op.Dd, w, op.n, h1, h2,
-                                                        tsign);
+                                                        tsign, op.h1f, op.h2f);
     return cudaGetLastError();
   }
 #define SBX_AX_CASE(NN)                                                                  \
@@ -474,8 +479,8 @@ cudaError_t launch_axhelm(const OpDev& op, const double* u, double* w, double h1
 cudaError_t launch_axhelm_diag(const OpDev& op, double h1, double h2, double* diag,
                                cudaStream_t s) {
   if (op.nodes == 0) return cudaSuccess;
-  ax_diag_kernel<<<(unsigned)((op.nodes + 255) / 256), 256, 0, s>>>(op.G, op.bm, op.Dd, op.n,
-                                                                   op.nodes, h1, h2, diag);
+  ax_diag_kernel<<<(unsigned)((op.nodes + 255) / 256), 256, 0, s>>>(
+      op.G, op.bm, op.Dd, op.n, op.nodes, h1, h2, diag, op.h1f, op.h2f);
   return cudaGetLastError();
 }
 

@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <memory>
 #include <random>
 #include <string>
 
@@ -181,6 +182,43 @@ int main(int argc, char** argv) {
     std::printf("%s device (fused sbx_pcg): %d iterations, rel %.9e, |x-x_cpu|/|x_cpu| %.2e\n",
                 tag, r_dev.iterations, r_dev.rel_residual, err);
     all_ok = all_ok && hyb_bitwise && dev_ok;
+  }
+  // 4. per-node coefficients (HelmholtzCoeffs::h1_field / h2_field): the
+  // reference pcg, all-CPU vs B200 operators through the adapter, bitwise;
+  // and the adapter's own solve (reference order on the device with fields)
+  {
+    Field h1f(GridTag::velocity, mesh.elem_count, basis.n());
+    Field h2f(GridTag::velocity, mesh.elem_count, basis.n());
+    std::uniform_real_distribution<double> d1(0.5, 2.0), d2(0.0, 3.0);
+    for (double& v : h1f.v) v = d1(rng);
+    for (double& v : h2f.v) v = d2(rng);
+    const HelmholtzCoeffs hf{1.0, 1.0, &h1f, &h2f};
+    HelmholtzOperator opf{&gf, &basis, &map, &mask, hf};
+    const Field diagf = opf.assembled_diagonal();
+    Field xc(GridTag::velocity, mesh.elem_count, basis.n());
+    const PcgResult rc = pcg([&](const Field& x, Field& y) { opf.apply(x, y); }, b,
+                             [&](const Field& r, Field& z) {
+                               z = r;
+                               for (std::size_t a = 0; a < r.v.size(); ++a)
+                                 z.v[a] = r.v[a] / diagf.v[a];
+                             },
+                             [&](const Field& u, const Field& v) {
+                               return field_dot_weighted(u, v, map.inv_mult);
+                             },
+                             cfg, xc);
+    sbx_sembox::Device dev(mesh, gf, basis, map, &mask);
+    Field xh(GridTag::velocity, mesh.elem_count, basis.n());
+    const PcgResult rh =
+        pcg(dev.apply_fn(hf, true), b, dev.jacobi_fn(hf), dev.dot_fn(true), cfg, xh);
+    Field xd(GridTag::velocity, mesh.elem_count, basis.n());
+    const PcgResult rd = dev.pcg(b, xd, cfg, hf, true, true);
+    const bool ok_h = rh.iterations == rc.iterations &&
+                      rh.residual_history == rc.residual_history && xh.v == xc.v;
+    const bool ok_d = rd.iterations == rc.iterations &&
+                      rd.residual_history == rc.residual_history && xd.v == xc.v;
+    std::printf("fields: cpu %d iterations; hybrid bitwise %s; device solve bitwise %s\n",
+                rc.iterations, ok_h ? "yes" : "NO", ok_d ? "yes" : "NO");
+    all_ok = all_ok && ok_h && ok_d;
   }
   std::printf("%s\n", all_ok ? "HYBRID PASS" : "HYBRID FAIL");
   return all_ok ? 0 : 1;
