@@ -25,10 +25,13 @@ def _port():
 def test_dist_check(cuda, ranks):
     if cuda.cuda.device_count() < ranks:
         pytest.skip(f"needs {ranks} GPUs")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
-           f"--nproc-per-node={ranks}", "--master-addr", "127.0.0.1", "--master-port",
-           str(_port()), os.path.join(ROOT, "tools", "dist_check.py")]
-    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    for _attempt in range(3):  # (a rendezvous port taken meanwhile: pick another)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={ranks}", "--master-addr", "127.0.0.1", "--master-port",
+               str(_port()), os.path.join(ROOT, "tools", "dist_check.py")]
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+        if out.returncode == 0 or "EADDRINUSE" not in out.stderr:
+            break
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
     assert out.stdout.count("ALL OK") == ranks
 
