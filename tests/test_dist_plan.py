@@ -136,14 +136,18 @@ def _worker(rank, world, port, q):
 @pytest.mark.parametrize("world", [2, 3, 8])
 def test_distributed_gs_plan_bitwise(world):
     ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    results = [q.get(timeout=300) for _ in range(world)]
-    for p in procs:
-        p.join(timeout=60)
+    for _attempt in range(3):  # (a rendezvous port taken meanwhile: pick another)
+        q = ctx.Queue()
+        port = _free_port()
+        procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+        for p in procs:
+            p.start()
+        results = [q.get(timeout=300) for _ in range(world)]
+        for p in procs:
+            p.join(timeout=60)
+        if not any("address already in use" in msg.lower() or "EADDRINUSE" in msg
+                   for _, msg in results):
+            break
     for rank, msg in results:
         assert msg == "ok", f"rank {rank}:\n{msg}"
 
