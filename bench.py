@@ -41,12 +41,15 @@ def unique_fraction(ex, ey, ez, N):
 
 def k1_geometry(N):
     """Which K1 variant the fused CG runs (mirrors launch_k1 in cg.cu): box
-    contexts with an even node count 8 <= n = N+1 <= 16 form the metric
-    on the fly from the trilinear map (56 B/node + 192 B/element streamed);
-    otherwise the 6 stored factors are streamed (104 B/node)."""
+    contexts with an even node count 8 <= n = N+1 <= 16, and n = 6 on the
+    tensor cores, form the metric on the fly from the trilinear map (56 B/node
+    + 192 B/element streamed); otherwise the 6 stored factors are streamed
+    (104 B/node)."""
     n = N + 1
     if (os.environ.get("SBX_STORED_GEOMETRY") or os.environ.get("SBX_NO_TMA") or n % 2
-            or n > 16 or n < 8):
+            or n > 16 or n < 6):
+        return "stored"
+    if n == 6 and (os.environ.get("SBX_K1_FMA") or os.environ.get("SBX_K1_FMA6")):
         return "stored"
     return "trilinear"
 
@@ -118,8 +121,13 @@ def bench_config(ex, ey, ez, N, iters, world):
 
 
 def k1_kernel_name(N):
-    if k1_geometry(N) == "trilinear" and N == 7 and not os.environ.get("SBX_K1_FMA"):
+    tc = k1_geometry(N) == "trilinear" and not os.environ.get("SBX_K1_FMA")
+    if tc and N == 7:
         return "k1_dmma_kernel (K1 on the FP64 tensor cores: p/x update + axhelm + p'Ap)"
+    if tc and N == 9:
+        return "k1_dmma10_kernel (K1 on the FP64 tensor cores, whole-element GEMMs)"
+    if tc and N == 5:
+        return "k1_dmmag_kernel<6> (K1 on the FP64 tensor cores, whole-element GEMMs)"
     return "ax_tma_kernel (K1: p/x update + axhelm + p'Ap)"
 
 

@@ -31,6 +31,7 @@
 #include "ax_tma.cuh"
 #include "ax_dmma.cuh"
 #include "ax_dmma10.cuh"
+#include "ax_dmmag.cuh"
 #include "cg.cuh"
 #include "dist_kern.cuh"
 #include "sbx_internal.h"
@@ -1279,6 +1280,41 @@ cudaError_t launch_k1_tma(const OpDev& op, const double* r, const double* dinv, 
   }
 }
 
+// K1 on the FP64 tensor cores at n = 6 (trilinear metric): ax_dmmag.cuh
+template <int n, bool HAS_DINV, bool HAS_BM>
+cudaError_t launch_k1_dmmag(const OpDev& op, const double* r, const double* dinv, double* p,
+                            double* x, double* w, double h1, double h2, CgScalars* sc,
+                            double* partials, cudaStream_t s, int dev) {
+  using Pol = CgK1Pol<HAS_DINV, HAS_BM>;
+  using Ch = DmmaGChoice<n, Pol::NV, dmmag_ovl<Pol>()>;
+  if constexpr (!Ch::ok) {
+    return cudaErrorNotSupported;
+  } else {
+    using L = DmmaGLayout<n, Pol::NV, Ch::TEAMS, Ch::S, dmmag_ovl<Pol>()>;
+    auto kern = k1_dmmag_kernel<n, Pol, Ch::TEAMS, Ch::S>;
+    static std::atomic<bool> attr_set[64];
+    if (!attr_set[dev & 63]) {
+      cudaError_t err =
+          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::smem);
+      if (err != cudaSuccess) return err;
+      attr_set[dev & 63] = true;
+    }
+    DParam<n> Dp;
+    for (int q = 0; q < n * n; ++q) Dp.d[q] = op.Dh[q];
+    QParam<n> Qp;
+    for (int q = 0; q < n; ++q) {
+      Qp.x[q] = op.Xh[q];
+      Qp.w[q] = op.Wh[q];
+    }
+    typename Pol::Args a{r, dinv, p, x, w, op.bm, h2, sc, op.dd, 0.0, 0.0, 0, 0, nullptr, 0};
+    a.multi = t_multi;
+    int64_t grid = num_sms(dev);
+    if (grid > op.E) grid = op.E;
+    return launch_pdl(kern, dim3((unsigned)grid, t_ncomp), L::threads, L::smem, s, a, op.tl,
+                      op.E, h1, Dp, partials, Qp);
+  }
+}
+
 // K1 on the FP64 tensor cores at n = 10 (trilinear metric): ax_dmma10.cuh
 template <bool HAS_DINV, bool HAS_BM>
 cudaError_t launch_k1_dmma10(const OpDev& op, const double* r, const double* dinv, double* p,
@@ -1404,6 +1440,21 @@ cudaError_t launch_k1(const OpDev& op, const double* r, const double* dinv, doub
           e = launch_k1_dmma10<true, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
         else
           e = launch_k1_dmma10<false, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
+      }
+    }
+    if constexpr (n == 6) {
+      // (the metric from the trilinear map: affordable on the tensor cores,
+      // not on the FMA pipe -- SBX_TRI_MINN keeps the FMA kernel on stored G)
+      static const bool fma6 = std::getenv("SBX_K1_FMA6") != nullptr;
+      if (op.tl && !stored && aligned16(op.tl) && !fma_k1 && !fma6) {
+        if (dinv && h2 != 0.0)
+          e = launch_k1_dmmag<6, true, true>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
+        else if (h2 != 0.0)
+          e = launch_k1_dmmag<6, false, true>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
+        else if (dinv)
+          e = launch_k1_dmmag<6, true, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
+        else
+          e = launch_k1_dmmag<6, false, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
       }
     }
     if (tri && e == cudaErrorNotSupported) e = go(std::true_type{});
