@@ -236,66 +236,86 @@ __global__ void __launch_bounds__(DmmaGLayout<n, Pol::NV, TEAMS, NSLOT, dmmag_ov
     }
     team_sync();
     // ---- trilinear metric, one lane per (i, j) column ---------------------
-    for (int col = tt; col < NN; col += TT) {
+    // (column constants: the adjugate rows are polynomials in t along a column)
+    struct ColC {
+      double A[3], B[3], Cc[3], Ev[3], P0[3], P1[3], P2[3], qa, qb, qc, wij;
+    };
+    auto col_consts = [&](int col, ColC& c) {
       const int j = col / n, i = col - n * j;
       const double* Gs = slot;
       const double ri = sQ[i], sj = sQ[j];
-      const double wij = h1 * (sQ[n + i] * sQ[n + j]);
-      double A[3], B[3], Cc[3], Ev[3], P0[3], P1[3], P2[3], qa, qb, qc;
-      {
-        auto cross = [](const double (&x)[3], const double (&y)[3], double (&o)[3]) {
-          o[0] = fma(x[1], y[2], -x[2] * y[1]);
-          o[1] = fma(x[2], y[0], -x[0] * y[2]);
-          o[2] = fma(x[0], y[1], -x[1] * y[0]);
-        };
-        double a0[3], b0[3], a1[3], b1[3], c2[3];
+      c.wij = h1 * (sQ[n + i] * sQ[n + j]);
+      auto cross = [](const double (&x)[3], const double (&y)[3], double (&o)[3]) {
+        o[0] = fma(x[1], y[2], -x[2] * y[1]);
+        o[1] = fma(x[2], y[0], -x[0] * y[2]);
+        o[2] = fma(x[0], y[1], -x[1] * y[0]);
+      };
+      double a0[3], b0[3], a1[3], b1[3], c2[3];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const double S0 = Gs[c], S1 = Gs[3 + c], S2 = Gs[6 + c], S01 = Gs[9 + c],
-                       S02 = Gs[12 + c], S12 = Gs[15 + c], S012 = Gs[18 + c];
-          a0[c] = fma(S01, sj, S0);
-          b0[c] = fma(S012, sj, S02);
-          a1[c] = fma(S01, ri, S1);
-          b1[c] = fma(S012, ri, S12);
-          c2[c] = fma(fma(S012, sj, S02), ri, fma(S12, sj, S2));
-        }
-        cross(a1, c2, A);
-        cross(b1, c2, B);
-        cross(c2, a0, Cc);
-        cross(c2, b0, Ev);
-        double u1[3], u2[3];
-        cross(a0, a1, P0);
-        cross(a0, b1, u1);
-        cross(b0, a1, u2);
-        cross(b0, b1, P2);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) P1[c] = u1[c] + u2[c];
-        qa = fma(a0[0], A[0], fma(a0[1], A[1], a0[2] * A[2]));
-        qb = fma(a0[0], B[0], fma(a0[1], B[1], fma(a0[2], B[2], fma(b0[0], A[0],
-             fma(b0[1], A[1], b0[2] * A[2])))));
-        qc = fma(b0[0], B[0], fma(b0[1], B[1], b0[2] * B[2]));
+      for (int q = 0; q < 3; ++q) {
+        const double S0 = Gs[q], S1 = Gs[3 + q], S2 = Gs[6 + q], S01 = Gs[9 + q],
+                     S02 = Gs[12 + q], S12 = Gs[15 + q], S012 = Gs[18 + q];
+        a0[q] = fma(S01, sj, S0);
+        b0[q] = fma(S012, sj, S02);
+        a1[q] = fma(S01, ri, S1);
+        b1[q] = fma(S012, ri, S12);
+        c2[q] = fma(fma(S012, sj, S02), ri, fma(S12, sj, S2));
       }
+      cross(a1, c2, c.A);
+      cross(b1, c2, c.B);
+      cross(c2, a0, c.Cc);
+      cross(c2, b0, c.Ev);
+      double u1[3], u2[3];
+      cross(a0, a1, c.P0);
+      cross(a0, b1, u1);
+      cross(b0, a1, u2);
+      cross(b0, b1, c.P2);
+#pragma unroll
+      for (int q = 0; q < 3; ++q) c.P1[q] = u1[q] + u2[q];
+      c.qa = fma(a0[0], c.A[0], fma(a0[1], c.A[1], a0[2] * c.A[2]));
+      c.qb = fma(a0[0], c.B[0], fma(a0[1], c.B[1], fma(a0[2], c.B[2], fma(b0[0], c.A[0],
+             fma(b0[1], c.A[1], b0[2] * c.A[2])))));
+      c.qc = fma(b0[0], c.B[0], fma(b0[1], c.B[1], b0[2] * c.B[2]));
+    };
+    auto metric_node = [&](const ColC& c, int off, double t, double wk) {
+      const double r = R[off], sv = Sx[off], tv = Tt[off];
+      double r0[3], r1[3], r2[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        r0[q] = fma(c.B[q], t, c.A[q]);
+        r1[q] = fma(c.Ev[q], t, c.Cc[q]);
+        r2[q] = fma(fma(c.P2[q], t, c.P1[q]), t, c.P0[q]);
+      }
+      const double det = fma(fma(c.qc, t, c.qb), t, c.qa);
+      const double f = (c.wij * wk) * fast_rcp(det);
+      double v[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) v[q] = fma(r, r0[q], fma(sv, r1[q], tv * r2[q]));
+      R[off] = f * fma(r0[0], v[0], fma(r0[1], v[1], r0[2] * v[2]));
+      Sx[off] = f * fma(r1[0], v[0], fma(r1[1], v[1], r1[2] * v[2]));
+      Tt[off] = f * fma(r2[0], v[0], fma(r2[1], v[1], r2[2] * v[2]));
+    };
+    // whole columns while every lane has one; a remainder that fits one round
+    // when split by plane (n = 6: 4 columns x 6 planes on 24 lanes) goes node
+    // by node instead of leaving the last round with 4 busy lanes
+    constexpr int FULL = NN / TT, LEFT = NN - FULL * TT;
+    constexpr bool SPLIT = LEFT > 0 && LEFT * n <= TT;
+    constexpr int COLS = SPLIT ? FULL * TT : NN;
+    for (int col = tt; col < COLS; col += TT) {
+      ColC c;
+      col_consts(col, c);
 #pragma unroll
       for (int k = 0; k < n; ++k) {
-        const int off = k * NN + col;
-        const double r = R[off], sv = Sx[off], tv = Tt[off];
-        const double t = Qp.x[k], wk = Qp.w[k];
-        double r0[3], r1[3], r2[3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          r0[c] = fma(B[c], t, A[c]);
-          r1[c] = fma(Ev[c], t, Cc[c]);
-          r2[c] = fma(fma(P2[c], t, P1[c]), t, P0[c]);
-        }
-        const double det = fma(fma(qc, t, qb), t, qa);
-        const double f = (wij * wk) * fast_rcp(det);
-        double v[3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) v[c] = fma(r, r0[c], fma(sv, r1[c], tv * r2[c]));
-        R[off] = f * fma(r0[0], v[0], fma(r0[1], v[1], r0[2] * v[2]));
-        Sx[off] = f * fma(r1[0], v[0], fma(r1[1], v[1], r1[2] * v[2]));
-        Tt[off] = f * fma(r2[0], v[0], fma(r2[1], v[1], r2[2] * v[2]));
+        metric_node(c, k * NN + col, Qp.x[k], Qp.w[k]);
         if ((k & 1) == 1) asm volatile("" ::: "memory");
+      }
+    }
+    if constexpr (SPLIT) {
+      if (tt < LEFT * n) {
+        const int col = COLS + tt / n, k = tt - n * (tt / n);
+        ColC c;
+        col_consts(col, c);
+        metric_node(c, k * NN + col, sQ[k], sQ[n + k]);
       }
     }
     team_sync();
