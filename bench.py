@@ -49,7 +49,7 @@ def k1_geometry(N):
     if (os.environ.get("SBX_STORED_GEOMETRY") or os.environ.get("SBX_NO_TMA") or n % 2
             or n > 16 or n < 6):
         return "stored"
-    if n == 6 and (os.environ.get("SBX_K1_FMA") or os.environ.get("SBX_K1_FMA6")):
+    if n == 6 and (os.environ.get("SBX_K1_FMA") or os.environ.get("SBX_K1_FMAG")):
         return "stored"
     return "trilinear"
 
@@ -126,8 +126,8 @@ def k1_kernel_name(N):
         return "k1_dmma_kernel (K1 on the FP64 tensor cores: p/x update + axhelm + p'Ap)"
     if tc and N == 9:
         return "k1_dmma10_kernel (K1 on the FP64 tensor cores, whole-element GEMMs)"
-    if tc and N == 5:
-        return "k1_dmmag_kernel<6> (K1 on the FP64 tensor cores, whole-element GEMMs)"
+    if tc and N in (5, 11) and not os.environ.get("SBX_K1_FMAG"):
+        return f"k1_dmmag_kernel<{N + 1}> (K1 on the FP64 tensor cores, whole-element GEMMs)"
     return "ax_tma_kernel (K1: p/x update + axhelm + p'Ap)"
 
 

@@ -1442,19 +1442,22 @@ cudaError_t launch_k1(const OpDev& op, const double* r, const double* dinv, doub
           e = launch_k1_dmma10<false, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
       }
     }
-    if constexpr (n == 6) {
-      // (the metric from the trilinear map: affordable on the tensor cores,
-      // not on the FMA pipe -- SBX_TRI_MINN keeps the FMA kernel on stored G)
-      static const bool fma6 = std::getenv("SBX_K1_FMA6") != nullptr;
-      if (op.tl && !stored && aligned16(op.tl) && !fma_k1 && !fma6) {
+    if constexpr (n == 6 || n == 12) {
+      // the generic whole-element DMMA kernel (n = 6: the metric from the
+      // trilinear map, affordable on the tensor cores but not on the FMA pipe
+      // -- SBX_TRI_MINN keeps the FMA kernel on stored G there; measured at
+      // 32^3: N = 11 37.2 vs 29.8 GDOF/s; N = 13, one team per SM by shared
+      // memory, 18.2 vs 32.7 on the FMA kernel, so n = 14 stays there)
+      static const bool fmag = std::getenv("SBX_K1_FMAG") != nullptr;
+      if (op.tl && !stored && aligned16(op.tl) && !fma_k1 && !fmag) {
         if (dinv && h2 != 0.0)
-          e = launch_k1_dmmag<6, true, true>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
+          e = launch_k1_dmmag<n, true, true>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
         else if (h2 != 0.0)
-          e = launch_k1_dmmag<6, false, true>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
+          e = launch_k1_dmmag<n, false, true>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
         else if (dinv)
-          e = launch_k1_dmmag<6, true, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
+          e = launch_k1_dmmag<n, true, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
         else
-          e = launch_k1_dmmag<6, false, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
+          e = launch_k1_dmmag<n, false, false>(op, r, dinv, p, x, w, h1, h2, sc, partials, s, dev);
       }
     }
     if (tri && e == cudaErrorNotSupported) e = go(std::true_type{});
