@@ -1183,6 +1183,10 @@ sbx_status sbx_debug_cg_k1(sbx_ctx* c, const double* u, double* w, double h1, do
     set_error("sbx_debug_cg_k1: single-process contexts only (K1 pushes the halo)");
     return SBX_E_CONFIG;
   }
+  if (c->op.h1f || c->op.h2f) {
+    set_error("sbx_debug_cg_k1: the fused K1 takes scalar h1 / h2 (per-node fields are set)");
+    return SBX_E_CONFIG;
+  }
   if (h2 != 0.0 && !c->op.bm) {
     set_error("sbx_debug_cg_k1: h2 != 0 needs the mass factors (bm)");
     return SBX_E_SHAPE;
