@@ -941,7 +941,7 @@ __global__ void __launch_bounds__(K2Layout<n, GROUPS, SPG>::threads, 1)
           // (an absent partner contributes +0.0 in the same position for
           // every copy) and IEEE addition is commutative, so every copy of a
           // node gets the same bits with no ordering logic.  Interface nodes
-          // (a copy on another rank) were assembled by dist_iface_kernel;
+          // (a copy on another rank) were assembled by k2_dist_prologue;
           // their partners were staged as zeros: own value only.
           double sum = (wo + wx) + (wy + wxy);
           if (k == 0) sum = sum + zs[0];
@@ -1625,17 +1625,16 @@ unsigned blocks_for(int64_t work, int threads, int64_t cap) {
   return (unsigned)b;
 }
 
-// One distributed CG iteration after K1: halo + p'Ap out, interface groups
-// and alpha in, K2, r'z/r'r all-reduce and the scalar step.
+// One distributed CG iteration after K1: the update kernel alone.  K1 (already
+// launched) put the halo on the wire from its epilogue; K2's head releases it
+// with this rank's p'Ap, waits for the peers', forms alpha and assembles the
+// interface groups (k2_dist_prologue); its last CTA leaves the r'z / r'r
+// partials for the next K1's head, which exchanges them and takes the scalar
+// step (k1_dist_head).
 cudaError_t dist_iteration_tail(const OpDev& op, const DistDev& D, double* w, double* r,
                                 const double* dinv, CgScalars* sc, double* partials,
                                 double* hist, int64_t hist_cap, cudaGraphConditionalHandle cond,
                                 int use_cond, cudaStream_t s) {
-  // K1 (already launched) put the halo on the wire from its epilogue and
-  // released phase 0; here: wait + alpha + interface groups, then K2 whose
-  // last CTA exchanges r'z / r'r and takes the scalar step.
-  // one thread per interface group: every group's chain of dependent loads
-  // (offsets -> codes -> local / NVLink copies) runs concurrently
   (void)D;
   return k2(op, w, r, dinv, sc, partials, hist, hist_cap, cond, use_cond, s);
 }
